@@ -1,0 +1,313 @@
+"""Benchmark: adaptive-AB3 Boussinesq steps on B200, Gcell-updates/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[4]): rip-current barred
+beach with a 68-component JONSWAP wavemaker, walls, quadratic friction,
+4096 x 4096 cells per GPU, fp64, real adaptive steps (Euler bootstrap then
+variable-step AB3 with cross-correction), synthetic bathymetry built by the
+reference's own generator restated (paper Eq. 48).  Every field is 134 MB,
+larger than the 126 MB L2, so no L2 flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  ``value``: cells x steps / device time with
+the state resident in HBM (CUDA events on the library stream, max over
+ranks).  ``e2e``: the same through the public ``Simulator`` API starting from
+host (pinned) buffers: initial state upload, K advance() calls (each: H2D
+step scalars, D2H reductions) and the final state download, all timed.
+``roofline``: the dominant kernel's algorithmic bytes / its event-timed
+duration vs the measured HBM copy bandwidth.  ``cpu_baseline``: the CPU
+oracle (C port of the reference step) on a bounded sample of the same
+workload.  ``--impl reference`` times that CPU implementation alone.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B_ALG_STEP = 424  # compulsory fp64 bytes per cell-update
+# algorithmic bytes per interior cell, per kernel launch
+KERNEL_BYTES = {
+    "stage": 8 * 29,    # R w,P,Q + 6 static + 10 history; W 5 stages + w* + U*,V* + 2 bases
+    "solve1": 8 * 12,   # per direction: R rhs + 4 LU factors, W result
+    "solve2": 8 * 20,   # per direction: R base, F*_n, first-solve field, 3 static, 4 LU; W result
+    "final": 8 * 7,     # R w*, bed_eff, P2, Q2; W w, P, Q
+    "ghost_t": 0, "ghost_n": 0,
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=5)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if r[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_baseline(case, steps: int, threads: int):
+    """Time the CPU oracle (C restatement of the reference step) on the
+    same case; returns Mcell-updates/s and the sample description."""
+    from oracle import oracle as orc
+    sim = orc.OracleSimulator(case.bathy, case.state.copy(), case.boundaries,
+                              orc.OController(dt_init=case.dt_init), phys=case.phys,
+                              h_dry=case.h_dry, threads=threads)
+    sim.advance()  # warm (page in, first touch)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sim.advance()
+    dt = time.perf_counter() - t0
+    cells = case.bathy.grid.nx * case.bathy.grid.ny
+    return cells * steps / dt / 1e9, dt
+
+
+def run_reference(args, case, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    threads = os.cpu_count() or 1
+    sim = orc.OracleSimulator(case.bathy, case.state.copy(), case.boundaries,
+                              orc.OController(dt_init=case.dt_init), phys=case.phys,
+                              h_dry=case.h_dry, threads=threads)
+    for _ in range(args.warmup):
+        sim.advance()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sim.advance()
+    wall = time.perf_counter() - t0
+    cells = case.bathy.grid.nx * case.bathy.grid.ny
+    v = cells * args.steps / wall / 1e9
+    line = {
+        "impl": "reference", "metric": "Gcell-updates/s", "value": v, "unit": "Gcell-updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, case),
+        "cpu_baseline": {"value": v, "unit": "Gcell-updates/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full steps of {config_dict(args, case)['workload']}"
+                                   " on the C oracle (OpenMP, bitwise = reference)"},
+        "e2e": {"value": v, "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, case):
+    g = case.bathy.grid
+    return {"workload": f"C5 rip channel + JONSWAP maker, {g.nx}x{g.ny} per GPU" if args.gpus == 1
+            else f"C5 rip channel, {g.nx}x{g.ny} per GPU x {args.gpus}",
+            "nx": g.nx, "ny": g.ny, "gpus": args.gpus, "precision": "fp64",
+            "solver": "thomas", "cross_correction": True, "adaptive": True,
+            "l2": "inputs larger than L2 (134 MB per field)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=1, help="divide the grid (debug only)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+
+    from paper_1909_04153_b200.scenario import make_case
+    case = make_case("C4", scale=args.scale)
+
+    if args.impl == "reference":
+        run_reference(args, case, rank)
+        return
+
+    import torch
+    from paper_1909_04153_b200 import stepper
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    cells = case.bathy.grid.nx * case.bathy.grid.ny
+
+    # ---- device-resident timing: value + per-kernel roofline ------------------
+    sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
+                            stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
+                            device=dev)
+    for _ in range(max(args.warmup, 3)):
+        sim.advance()
+    stream = sim._dev.stream
+    sim._dev.set_timing(True)
+    per_kernel = {}
+    clocks = ClockSampler(dev.index)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(args.steps):
+        sim.advance()
+        for name, ms in sim._dev.kernel_times():
+            per_kernel.setdefault(name, []).append(ms)
+    end.record(stream)
+    torch.cuda.synchronize(dev)
+    clock_info = clocks.stop()
+    ms_total = start.elapsed_time(end)
+    if dist is not None:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        dist.barrier()
+    sim._dev.set_timing(False)
+    ms_step = ms_total / args.steps
+    value = cells * world * args.steps / (ms_total * 1e-3) / 1e9
+    kps = sim._dev.kernels_per_step()
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
+
+    hbm, peak_kind = peaks()
+    avg = {k: float(np.mean(v)) for k, v in per_kernel.items()}
+    dom = max((k for k in avg if k in KERNEL_BYTES and KERNEL_BYTES[k] > 0), key=lambda k: avg[k])
+    bytes_launch = KERNEL_BYTES[dom] * cells
+    achieved = bytes_launch / (avg[dom] * 1e-3) / 1e9
+    step_gbs = value / world * B_ALG_STEP
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                "kernel_ms": avg, "step_achieved": step_gbs, "step_frac": step_gbs / hbm,
+                "step_bytes_per_cell": B_ALG_STEP}
+
+    # ---- e2e through the public API from pinned host buffers --------------------
+    import torch as _t
+    pin = [_t.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+           for a in (case.state.w, case.state.p, case.state.q)]
+    from paper_1909_04153_b200.grid import FieldState
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    sim = stepper.Simulator(case.bathy, FieldState(*pin), case.boundaries,
+                            stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
+                            device=dev)
+    t_setup = time.perf_counter()
+    sim.state = FieldState(*pin)  # the upload proper
+    for _ in range(args.steps):
+        sim.advance()
+    final = sim.state
+    t1 = time.perf_counter()
+    e2e_s = t1 - t_setup
+    if dist is not None:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    state_bytes = 3 * final.w.nbytes
+    import ctypes
+    from paper_1909_04153_b200 import _native as nat
+    h2d = state_bytes / args.steps + ctypes.sizeof(nat.StepParams)
+    d2h = state_bytes / args.steps + ctypes.sizeof(nat.StepResult)
+    e2e = {"value": cells * world * args.steps / e2e_s / 1e9, "unit": "Gcell-updates/s",
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+           "includes": "state upload from pinned host + K advance() (H2D scalars, D2H "
+                       "reductions) + final state download; excludes one-time setup "
+                       f"({t_setup - t0:.2f} s: static upload + LU factorization)"}
+    sim.close()
+
+    # ---- CPU baseline (rank 0, N = 1 only) ------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        v_cpu, wall = cpu_baseline(case, args.cpu_steps, threads)
+        cpu = {"value": v_cpu, "unit": "Gcell-updates/s", "cores": threads, "kind": "port",
+               "sample": f"{args.cpu_steps} full {case.bathy.grid.nx}x{case.bathy.grid.ny} steps "
+                         f"(after 1 warm-up) of the same case on the C oracle, {wall:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "Gcell-updates/s", "value": value, "unit": "Gcell-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (rip-channel bathymetry, JONSWAP maker; reference generators)",
+            "config": config_dict(args, case), "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": kps * args.steps, "clocks": clock_info,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/*
+ * bsq.h -- C ABI of the B200-native adaptive-AB3 Boussinesq step.
+ *
+ * The library replaces the per-step compute of the reference solver's step
+ * loop, boussim.stepper.Simulator._advance
+ * (/root/reference/pkg/src/boussim/stepper.py:225-325), and the numba
+ * kernels it calls (/root/reference/pkg/src/boussim/_kernels.py:20-451).
+ * The host (paper_1909_04153_b200/stepper.py, a drop-in for
+ * boussim.stepper.Simulator) keeps the controller and evaluates the handful
+ * of fp64 scalars per step; everything per cell runs in sm_100a kernels.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Host arrays are float64, row-major,
+ *     in the reference's padded layout: fields (ny+4) x (nx+4),
+ *     bed_face_x (ny+4) x (nx+3), bed_face_y (ny+3) x (nx+4); interior
+ *     arrays ny x nx (grid.py:1-20).
+ *   - Device memory is owned by the caller: bsq_workspace_bytes() says how
+ *     much, bsq_create() carves its buffers out of that one allocation (the
+ *     Python host passes a torch-owned CUDA tensor).  The library never
+ *     allocates device memory itself.
+ *   - All device work runs on the stream given to bsq_create (NULL: the
+ *     library creates a non-blocking stream).  Calls that return host
+ *     results synchronize that stream before returning.
+ *   - Side order everywhere is north, south, east, west (boundary.py:25).
+ *   - Every entry point returns a bsq_status; bsq_last_error() describes
+ *     the most recent failure on the calling thread.
+ */
+#ifndef BSQ_H
+#define BSQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BSQ_OK = 0,
+    BSQ_ERR_BAD_ARG = 1,  /* -> ValueError */
+    BSQ_ERR_CUDA = 2,     /* -> RuntimeError */
+    BSQ_ERR_SINGULAR = 3, /* -> ZeroDivisionError (_kernels.py:369-376) */
+    BSQ_ERR_NO_DEVICE = 4,
+    BSQ_ERR_NCCL = 5
+} bsq_status;
+
+enum { BSQ_SIDE_NORTH = 0, BSQ_SIDE_SOUTH = 1, BSQ_SIDE_EAST = 2, BSQ_SIDE_WEST = 3 };
+enum { BSQ_WALL = 0, BSQ_MAKER = 1, BSQ_SPONGE = 2 }; /* sponge ghosts mirror like a wall */
+enum { BSQ_FP64 = 0, BSQ_FP32 = 1 };
+enum { BSQ_THOMAS = 0, BSQ_CR = 1 };
+
+/* Grid, physics and scheme constants.  Derived constants are passed in,
+ * computed by the host exactly as the reference's Python computes them
+ * (e.g. dx2 = dx**2, bp13 = b_disp + 1.0/3.0), so the device never
+ * re-derives a value that could round differently. */
+typedef struct {
+    int32_t nx, ny;            /* interior cells */
+    int32_t precision;         /* BSQ_FP64 (bitwise parity) or BSQ_FP32 */
+    int32_t solver;            /* BSQ_THOMAS */
+    int32_t side_kind[4];      /* BSQ_WALL / BSQ_MAKER / BSQ_SPONGE per side */
+    int32_t cross_correction;  /* re-solve with exact cross increment (stepper.py:262-280) */
+    int32_t sponge_lo[4];      /* first band cell index (col for E/W, row for N/S) */
+    int32_t sponge_len[4];     /* band length, 0 = none */
+    double dx, dy, dx2, dy2;
+    double g, b_disp, bp13, c_f, theta, h_eps, h_dry, ws;
+} bsq_desc;
+
+/* Static fields (host pointers, reference layout; copied at create). */
+typedef struct {
+    const double *bed_eff, *depth, *depth_dx, *depth_dy; /* (ny+4) x (nx+4) */
+    const double *bed_face_x;                            /* (ny+4) x (nx+3) */
+    const double *bed_face_y;                            /* (ny+3) x (nx+4) */
+} bsq_static;
+
+/* Per-step host scalars (stepper.py:239-254; multistep.py:118-228;
+ * boundary.py:190-199, 264-300). */
+typedef struct {
+    double t, dt;
+    int32_t euler;            /* 1: bootstrap step (step_index < 3) */
+    int32_t reserved;
+    double wc, wp, wp2;       /* ab3_weights, ratio_policy="clamp" */
+    double sc, sp, sp2;       /* increment_weights */
+    double maker_eta_t[4], maker_flux_t[4]; /* maker_surface_flux at t     */
+    double maker_eta_n[4], maker_flux_n[4]; /* maker_surface_flux at t+dt */
+    const double *sponge_fac[4];            /* host, sponge_len[s] factors exp(-lambda dt) */
+} bsq_step_params;
+
+/* Per-step device reductions, returned to the host. */
+typedef struct {
+    double max_rate, max_speed, max_depth; /* speed_extrema of the new state (_kernels.py:324-353) */
+    double max_dev;                        /* max |w - max(ws, bed_eff)|; NaN if w non-finite */
+    double clamped;                        /* sum max(bed_eff - w_pred, 0) over the interior */
+    int64_t stage_bad[5]; /* first row-major interior index of a non-finite e,f,g,fstar,gstar, or -1 */
+    int64_t state_bad[3]; /* same for w, P, Q of the new state */
+} bsq_step_result;
+
+typedef struct bsq_ctx bsq_ctx;
+
+/* -- lifecycle ---------------------------------------------------------- */
+size_t bsq_workspace_bytes(const bsq_desc *desc);
+int bsq_create(const bsq_desc *desc, const bsq_static *fields, void *workspace, size_t bytes,
+               void *stream, bsq_ctx **out);
+int bsq_destroy(bsq_ctx *ctx);
+const char *bsq_last_error(void);
+int bsq_device_count(int *count);
+
+/* -- state / history I/O (host buffers, reference layout) ------------------ */
+int bsq_upload_state(bsq_ctx *ctx, const double *w, const double *p, const double *q);
+/* which: 0 = committed state, 1 = pending new state of the last bsq_step */
+int bsq_download_state(bsq_ctx *ctx, int which, double *w, double *p, double *q);
+/* level 0 = newest committed stage set; field 0..4 = e, f, g, fstar, gstar */
+int bsq_download_history(bsq_ctx *ctx, int level, int field, double *out);
+
+/* -- the step ----------------------------------------------------------- */
+/* Runs stepper.py:233-305 on the device into pending buffers and returns
+ * the reductions the host controller needs.  Nothing is committed. */
+int bsq_step(bsq_ctx *ctx, const bsq_step_params *params, bsq_step_result *result);
+/* Accept the pending step: state <- new state, history ring advances. */
+int bsq_commit(bsq_ctx *ctx);
+
+/* -- kernel-level seams (per-kernel parity tests) -------------------------- */
+/* stage set E,F,G,F*,G* of the committed state as it is (no ghost fill) */
+int bsq_stage_rates(bsq_ctx *ctx, double *e, double *f, double *g, double *fstar,
+                    double *gstar);
+/* implicit.solve_momentum (implicit.py:197-205) with the device solver */
+int bsq_solve_momentum(bsq_ctx *ctx, const double *ustar, const double *vstar,
+                       const double *pg_west, const double *pg_east, const double *qg_south,
+                       const double *qg_north, double *p_out, double *q_out);
+/* hydro.speed_extrema of the committed state: {max_rate, max_speed, max_depth} */
+int bsq_speed_extrema(bsq_ctx *ctx, double *out3);
+/* Boundaries.apply_ghosts on the committed state with maker values */
+int bsq_fill_ghosts(bsq_ctx *ctx, const double *maker_eta, const double *maker_flux);
+
+/* -- timing support ------------------------------------------------------ */
+/* When enabled, bsq_step brackets each kernel with CUDA events on the
+ * library stream; bsq_kernel_times returns the last step's per-kernel
+ * device times (ms) and names, in launch order. */
+int bsq_set_timing(bsq_ctx *ctx, int enable);
+int bsq_kernel_times(bsq_ctx *ctx, int max_n, float *ms, const char **names, int *n_out);
+/* number of kernels one bsq_step launches */
+int bsq_kernels_per_step(bsq_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSQ_H */

@@ -1,0 +1,116 @@
+"""ctypes binding of libbsq.so (include/bsq.h).
+
+There is no fallback: importing the step without the built library, or
+creating a context without a CUDA device, raises.  Build with
+``python -m paper_1909_04153_b200.build`` (``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libbsq.so")
+
+BSQ_OK, BSQ_ERR_BAD_ARG, BSQ_ERR_CUDA, BSQ_ERR_SINGULAR, BSQ_ERR_NO_DEVICE, BSQ_ERR_NCCL = range(6)
+WALL, MAKER, SPONGE = 0, 1, 2
+FP64, FP32 = 0, 1
+THOMAS, CR = 0, 1
+
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+class Desc(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32),
+                ("precision", ctypes.c_int32), ("solver", ctypes.c_int32),
+                ("side_kind", ctypes.c_int32 * 4), ("cross_correction", ctypes.c_int32),
+                ("sponge_lo", ctypes.c_int32 * 4), ("sponge_len", ctypes.c_int32 * 4),
+                ("dx", ctypes.c_double), ("dy", ctypes.c_double),
+                ("dx2", ctypes.c_double), ("dy2", ctypes.c_double),
+                ("g", ctypes.c_double), ("b_disp", ctypes.c_double), ("bp13", ctypes.c_double),
+                ("c_f", ctypes.c_double), ("theta", ctypes.c_double), ("h_eps", ctypes.c_double),
+                ("h_dry", ctypes.c_double), ("ws", ctypes.c_double)]
+
+
+class Static(ctypes.Structure):
+    _fields_ = [("bed_eff", _dp), ("depth", _dp), ("depth_dx", _dp), ("depth_dy", _dp),
+                ("bed_face_x", _dp), ("bed_face_y", _dp)]
+
+
+class StepParams(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_double), ("dt", ctypes.c_double),
+                ("euler", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("wc", ctypes.c_double), ("wp", ctypes.c_double), ("wp2", ctypes.c_double),
+                ("sc", ctypes.c_double), ("sp", ctypes.c_double), ("sp2", ctypes.c_double),
+                ("maker_eta_t", ctypes.c_double * 4), ("maker_flux_t", ctypes.c_double * 4),
+                ("maker_eta_n", ctypes.c_double * 4), ("maker_flux_n", ctypes.c_double * 4),
+                ("sponge_fac", _dp * 4)]
+
+
+class StepResult(ctypes.Structure):
+    _fields_ = [("max_rate", ctypes.c_double), ("max_speed", ctypes.c_double),
+                ("max_depth", ctypes.c_double), ("max_dev", ctypes.c_double),
+                ("clamped", ctypes.c_double),
+                ("stage_bad", ctypes.c_int64 * 5), ("state_bad", ctypes.c_int64 * 3)]
+
+
+# every symbol include/bsq.h declares: (name, restype, argtypes)
+SIGNATURES = [
+    ("bsq_workspace_bytes", ctypes.c_size_t, [ctypes.POINTER(Desc)]),
+    ("bsq_create", ctypes.c_int, [ctypes.POINTER(Desc), ctypes.POINTER(Static), ctypes.c_void_p,
+                                  ctypes.c_size_t, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    ("bsq_destroy", ctypes.c_int, [ctypes.c_void_p]),
+    ("bsq_last_error", ctypes.c_char_p, []),
+    ("bsq_device_count", ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    ("bsq_upload_state", ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp]),
+    ("bsq_download_state", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _dp, _dp, _dp]),
+    ("bsq_download_history", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _dp]),
+    ("bsq_step", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(StepParams),
+                                ctypes.POINTER(StepResult)]),
+    ("bsq_commit", ctypes.c_int, [ctypes.c_void_p]),
+    ("bsq_stage_rates", ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, _dp, _dp]),
+    ("bsq_solve_momentum", ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
+    ("bsq_speed_extrema", ctypes.c_int, [ctypes.c_void_p, _dp]),
+    ("bsq_fill_ghosts", ctypes.c_int, [ctypes.c_void_p, _dp, _dp]),
+    ("bsq_set_timing", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    ("bsq_kernel_times", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_float),
+                                        ctypes.POINTER(ctypes.c_char_p),
+                                        ctypes.POINTER(ctypes.c_int)]),
+    ("bsq_kernels_per_step", ctypes.c_int, [ctypes.c_void_p]),
+]
+
+_lib = None
+
+
+def lib():
+    """The loaded library; raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_1909_04153_b200.build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def ptr(a):
+    return a.ctypes.data_as(_dp)
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == BSQ_OK:
+        return
+    msg = lib().bsq_last_error().decode(errors="replace")
+    if rc == BSQ_ERR_SINGULAR:
+        raise ZeroDivisionError(msg)
+    if rc == BSQ_ERR_BAD_ARG:
+        raise ValueError(f"{what}: {msg}" if what else msg)
+    raise RuntimeError(f"libbsq error {rc} in {what}: {msg}")

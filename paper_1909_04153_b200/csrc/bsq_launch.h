@@ -1,0 +1,61 @@
+// bsq_launch.h -- kernel argument bundles and launchers (host-visible).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "bsq_device.cuh"
+
+namespace bsq {
+
+template <class T>
+struct StagePtrs {
+    const T *w, *p, *q;             // committed state, ghost-filled at t
+    const T *be, *dep, *ddx, *ddy;  // static fields
+    const T *bfx, *bfy;
+    T *h0[5];                       // new stage set e, f, g, fstar, gstar
+    const T *h1[5], *h2[5];         // previous two levels (AB3 only)
+    T *wn;                          // predicted w -> pending state's w
+    T *bu, *bv, *us, *vs;           // quadrature bases and predicted U*, V*
+    unsigned long long *bad;        // [5] first non-finite stage cell
+};
+
+template <class T>
+struct SolvePtrs {
+    const T *rx, *ry;               // phase 1: us, vs;  phase 2: base_u, base_v
+    const T *fs, *gs;               // phase 2: stored F*_n, G*_n
+    const T *q1, *p1;               // phase 2: first-solve Q (for F*) and P (for G*)
+    const T *dep, *ddx, *ddy;
+    const T *gp, *gq;               // arrays holding the P / Q ghost values used for folding
+    const T *ax, *denx, *rdenx, *cwx, *cx_last;
+    const T *ay, *deny, *rdeny, *cwy, *cy_last;
+    T *scrx, *scry;                 // forward-sweep scratch
+    T *outx, *outy;                 // solved P (rows) and Q (columns)
+};
+
+template <class T>
+struct FinalPtrs {
+    T *w;                           // predicted w in, final w out (pending state)
+    const T *pin, *qin;             // solved momenta
+    T *pout, *qout;                 // pending state's P, Q
+    const T *be;
+    const T *fac[4];                // sponge factors per side
+    Partial *part;
+    unsigned int *counter;
+    DevResult *res;
+};
+
+template <class T>
+void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
+                  const T *sq, T *dw, T *dp, T *dq, cudaStream_t st);
+template <class T>
+void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
+                  cudaStream_t st);
+template <class T>
+void launch_solve(const Consts<T> &C, const SolvePtrs<T> &S, int phase, cudaStream_t st);
+template <class T>
+void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st);
+template <class T>
+void launch_extrema(const Consts<T> &C, const T *w, const T *p, const T *q, const T *be,
+                    Partial *part, cudaStream_t st);
+int final_blocks(int nx, int ny);
+
+}  // namespace bsq
