@@ -317,12 +317,184 @@ __device__ __forceinline__ T cross_g(const Consts<T> &C, const T *p, long o, T d
     return sixth * (dx_ * p_y + dy_ * p_x) + d2 * p_xy;
 }
 
-// One thread per line.  Blocks [0, nbx) take x lines (rows, P); blocks
-// [nbx, ...) take y lines (columns, Q).  The LU factors of the static
-// operator are precomputed on the host with thomas_batch's own arithmetic
-// (den_i = b_i - a_i cw_{i-1}, cw_i = c_i / den_i), so the per-step forward
-// sweep dw_i = (r_i - a_i dw_{i-1}) / den_i and back substitution
-// x_i = dw_i - cw_i x_{i+1} reproduce thomas_batch bit for bit.
+// Warp-specialized pipelined line solve.
+//
+// A CTA owns 32 lines (x: 32 consecutive rows; y: 32 consecutive columns).
+// Warp 0 is the consumer: lane l runs line l's Thomas recurrence entirely
+// out of shared memory.  Warps 1..7 are producers: per chunk of SK elements
+// they stream the inputs with coalesced loads (a row segment for x, a
+// 32-column row slice for y), assemble the folded right-hand side -- for
+// phase 2 including the cross-correction F*(P1,Q1) stencil -- and write the
+// consumer's results back.  Chunks are double buffered: while the consumer
+// sweeps chunk c, producers fill chunk c+1 and drain chunk c-1.
+//
+// The LU factors of the static operator are precomputed on the host with
+// thomas_batch's own arithmetic (den_i = b_i - a_i cw_{i-1},
+// cw_i = c_i / den_i), so the per-step forward sweep
+// dw_i = (r_i - a_i dw_{i-1}) / den_i and back substitution
+// x_i = dw_i - cw_i x_{i+1} reproduce thomas_batch bit for bit.  The forward
+// sweep's dw is parked in the output array and overwritten by x.
+constexpr int SK = 32;           // chunk length (elements per line)
+constexpr int SLD = SK + 1;      // padded smem row: conflict-free column access
+constexpr int SW = 8;            // warps per CTA (1 consumer + 7 producers)
+constexpr int SBUF = 32 * SLD;   // one [32][SLD] tile
+
+template <class T>
+struct SolveSmem {
+    T r[2][SBUF], a[2][SBUF], den[2][SBUF], rden[2][SBUF], out[2][SBUF];
+};
+
+template <class T, bool XDIR>
+__device__ __forceinline__ int tile_idx(int line, int k) {
+    // x: [line][k] so a producer warp writes one row segment contiguously and
+    //    the consumer reads a column (padded stride: conflict-free)
+    // y: [k][line] so both sides touch 32 consecutive doubles
+    return XDIR ? line * SLD + k : k * SLD + line;
+}
+
+template <class T, bool XDIR>
+__device__ __forceinline__ long line_off(const Layout &L, int line, int k) {
+    return XDIR ? L.at(GL + line, GL + k) : L.at(GL + k, GL + line);
+}
+
+template <class T, bool XDIR, int PHASE>
+__device__ void solve_lines(const Consts<T> &C, const SolvePtrs<T> &S, int line0, SolveSmem<T> &sm) {
+    const Layout L = C.L;
+    const int n = XDIR ? L.nx : L.ny;           // line length
+    const int nlines = XDIR ? L.ny : L.nx;
+    const int nc = (n + SK - 1) / SK;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ptid = threadIdx.x - 32, np = (SW - 1) * 32;
+    const T *rhs = XDIR ? S.rx : S.ry;
+    const T *A = XDIR ? S.ax : S.ay;
+    const T *DEN = XDIR ? S.denx : S.deny;
+    const T *RDEN = XDIR ? S.rdenx : S.rdeny;
+    const T *CW = XDIR ? S.cwx : S.cwy;
+    const T *clast = XDIR ? S.cx_last : S.cy_last;
+    T *out = XDIR ? S.outx : S.outy;
+
+    // item -> (line, k) so consecutive producer lanes touch consecutive addresses
+    auto item = [&](int it, int &ln, int &k) {
+        if (XDIR) { ln = it >> 5; k = it & 31; } else { k = it >> 5; ln = it & 31; }
+    };
+
+    auto fill_fwd = [&](int c, int b) {
+        for (int it = ptid; it < 32 * SK; it += np) {
+            int ln, k;
+            item(it, ln, k);
+            const int line = line0 + ln, e = c * SK + k;
+            const int t = tile_idx<T, XDIR>(ln, k);
+            if (line >= nlines || e >= n) {
+                sm.r[b][t] = T(0); sm.a[b][t] = T(0); sm.den[b][t] = T(1); sm.rden[b][t] = T(1);
+                continue;
+            }
+            const long o = line_off<T, XDIR>(L, line, e);
+            T r;
+            if (PHASE == 1) {
+                r = rhs[o];
+            } else {  // us_corr = base + (F*(P1, Q1) - F*_n)   (stepper.py:272-273)
+                T cr = XDIR ? cross_f(C, S.q1, o, S.dep[o], S.ddx[o], S.ddy[o])
+                            : cross_g(C, S.p1, o, S.dep[o], S.ddx[o], S.ddy[o]);
+                r = rhs[o] + (cr - (XDIR ? S.fs[o] : S.gs[o]));
+            }
+            const T a = A[o];
+            if (e == 0) {  // implicit.py:178 / :190 ghost folding
+                const T g0 = XDIR ? S.gp[L.at(GL + line, GL - 1)] : S.gq[L.at(GL - 1, GL + line)];
+                r = r - a * g0;
+            }
+            if (e == n - 1) {
+                const T g1 = XDIR ? S.gp[L.at(GL + line, n + GL)] : S.gq[L.at(n + GL, GL + line)];
+                r = r - clast[line] * g1;
+            }
+            sm.r[b][t] = r;
+            sm.a[b][t] = a;
+            sm.den[b][t] = DEN[o];
+            sm.rden[b][t] = RDEN[o];
+        }
+    };
+    auto drain = [&](int c, int b) {  // out tile -> global
+        for (int it = ptid; it < 32 * SK; it += np) {
+            int ln, k;
+            item(it, ln, k);
+            const int line = line0 + ln, e = c * SK + k;
+            if (line < nlines && e < n) out[line_off<T, XDIR>(L, line, e)] = sm.out[b][tile_idx<T, XDIR>(ln, k)];
+        }
+    };
+    auto fill_bwd = [&](int c, int b) {  // dw (parked in out) and cw
+        for (int it = ptid; it < 32 * SK; it += np) {
+            int ln, k;
+            item(it, ln, k);
+            const int line = line0 + ln, e = c * SK + k;
+            const int t = tile_idx<T, XDIR>(ln, k);
+            if (line >= nlines || e >= n) {
+                sm.r[b][t] = T(0); sm.a[b][t] = T(0);
+                continue;
+            }
+            const long o = line_off<T, XDIR>(L, line, e);
+            sm.r[b][t] = out[o];
+            sm.a[b][t] = CW[o];
+        }
+    };
+
+    // ---- forward sweep -------------------------------------------------------
+    if (warp > 0) fill_fwd(0, 0);
+    __syncthreads();
+    T dw = T(0);
+    for (int c = 0; c < nc; c++) {
+        const int b = c & 1;
+        if (warp == 0) {
+            const int kmax = min(SK, n - c * SK);
+            for (int k = 0; k < kmax; k++) {
+                const int t = tile_idx<T, XDIR>(lane, k);
+                const T r = sm.r[b][t];
+                const T num = (c == 0 && k == 0) ? r : r - sm.a[b][t] * dw;
+                dw = div_static(num, sm.den[b][t], sm.rden[b][t]);
+                sm.out[b][t] = dw;
+            }
+        } else {
+            if (c + 1 < nc) fill_fwd(c + 1, b ^ 1);
+            if (c >= 1) drain(c - 1, b ^ 1);
+        }
+        __syncthreads();
+    }
+    if (warp > 0) drain(nc - 1, (nc - 1) & 1);
+    __syncthreads();
+
+    // ---- back substitution (chunks in reverse) -------------------------------
+    if (warp > 0) fill_bwd(nc - 1, 0);
+    __syncthreads();
+    T xv = T(0);
+    for (int s = 0; s < nc; s++) {
+        const int c = nc - 1 - s, b = s & 1;
+        if (warp == 0) {
+            const int kmax = min(SK, n - c * SK);
+            for (int k = kmax - 1; k >= 0; k--) {
+                const int t = tile_idx<T, XDIR>(lane, k);
+                xv = (s == 0 && k == kmax - 1) ? sm.r[b][t] : sm.r[b][t] - sm.a[b][t] * xv;
+                sm.out[b][t] = xv;
+            }
+        } else {
+            if (s + 1 < nc) fill_bwd(c - 1, b ^ 1);
+            if (s >= 1) drain(c + 1, b ^ 1);
+        }
+        __syncthreads();
+    }
+    if (warp > 0) drain(0, (nc - 1) & 1);
+}
+
+// Blocks [0, nbx) take x lines (rows -> P); blocks [nbx, ...) y lines (columns -> Q).
+template <class T, int PHASE>
+__global__ void __launch_bounds__(SW * 32, 2) k_solve_pipe(Consts<T> C, SolvePtrs<T> S, int nbx) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SolveSmem<T> &sm = *reinterpret_cast<SolveSmem<T> *>(smem_raw);
+    if ((int)blockIdx.x < nbx)
+        solve_lines<T, true, PHASE>(C, S, blockIdx.x * 32, sm);
+    else
+        solve_lines<T, false, PHASE>(C, S, (blockIdx.x - nbx) * 32, sm);
+}
+
+// Reference single-thread-per-line variant (kept for A/B timing; not launched
+// by the step).
 template <class T>
 __global__ void __launch_bounds__(64) k_solve(Consts<T> C, SolvePtrs<T> S, int phase, int nbx) {
     const Layout L = C.L;
@@ -594,6 +766,26 @@ void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A,
 
 template <class T>
 void launch_solve(const Consts<T> &C, const SolvePtrs<T> &S, int phase, cudaStream_t st) {
+    const int nbx = (C.L.ny + 31) / 32, nby = (C.L.nx + 31) / 32;
+    const size_t smem = sizeof(SolveSmem<T>);
+    static bool attr_set[2] = {false, false};
+    if (phase == 1) {
+        if (!attr_set[0]) {
+            cudaFuncSetAttribute(k_solve_pipe<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_set[0] = true;
+        }
+        k_solve_pipe<T, 1><<<nbx + nby, SW * 32, smem, st>>>(C, S, nbx);
+    } else {
+        if (!attr_set[1]) {
+            cudaFuncSetAttribute(k_solve_pipe<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_set[1] = true;
+        }
+        k_solve_pipe<T, 2><<<nbx + nby, SW * 32, smem, st>>>(C, S, nbx);
+    }
+}
+
+template <class T>
+void launch_solve_simple(const Consts<T> &C, const SolvePtrs<T> &S, int phase, cudaStream_t st) {
     const int bs = 64;
     int nbx = (C.L.ny + bs - 1) / bs, nby = (C.L.nx + bs - 1) / bs;
     k_solve<T><<<nbx + nby, bs, 0, st>>>(C, S, phase, nbx);
