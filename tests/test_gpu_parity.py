@@ -216,19 +216,28 @@ def test_nonfinite_state_aborts_with_location():
     z = gc.load("hump")
     bathy, state, bounds, phys, ckw, skw = gc.inputs(z)
     sim = stepper.Simulator(bathy, state, bounds, stepper.TimeController(**ckw), phys=phys)
+    ora = orc.OracleSimulator(bathy, gc.inputs(z)[1], bounds, orc.OController(**ckw), phys=phys)
     sim.advance()
-    sim.state.p[GHOST + 2, GHOST + 3] = np.inf
-    with pytest.raises(stepper.InstabilityError, match=r"j=2, i=3"):
+    ora.advance()
+    sim.state.p[GHOST + 2, GHOST + 3] = np.inf   # edit the host copy, as the reference test does
+    st = ora.state
+    st.p[GHOST + 2, GHOST + 3] = np.inf
+    ora.set_state(st)
+    with pytest.raises(orc.OracleInstability) as want:
+        ora.advance()
+    with pytest.raises(stepper.InstabilityError) as got:
         sim.advance()
+    # the first non-finite stage cell in row-major order, as the reference reports it
+    assert str(got.value) == str(want.value)
+    assert got.value.step_index == want.value.step_index == 2
 
 
 def test_singular_operator_raises_zero_division():
     grid = Grid(8, 6, 1.0, 1.0)
     from paper_1909_04153_b200.grid import build_bathymetry
     bathy = build_bathymetry(grid, np.full((6, 8), -1.0), ws=0.0)
-    # B = -1/3 makes the operator the identity minus nothing... pick b_disp so b == 0:
-    # b = 1 + 2 (B + 1/3) d^2/dx^2 = 0  ->  B + 1/3 = -0.5
-    phys = PhysParams(b_disp=-0.5 - 1.0 / 3.0)
+    # b = 1 + 2 (B + 1/3) d^2/dx^2 is exactly 0 for this B (d = dx = 1)
+    phys = PhysParams(b_disp=-0.8333333333333334)
     walls = bc.Boundaries(west=bc.Wall(), east=bc.Wall(), south=bc.Wall(), north=bc.Wall())
     with pytest.warns(UserWarning):
         sim = stepper.Simulator(bathy, FieldState(*[a.copy() for a in (
