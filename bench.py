@@ -41,7 +41,8 @@ B_ALG_STEP = 424  # compulsory fp64 bytes per cell-update
 KERNEL_BYTES = {
     "stage": 8 * 29,    # R w,P,Q + 6 static + 10 history; W 5 stages + w* + U*,V* + 2 bases
     "solve1": 8 * 12,   # per direction: R rhs + 4 LU factors, W result
-    "solve2": 8 * 20,   # per direction: R base, F*_n, first-solve field, 3 static, 4 LU; W result
+    "correct": 8 * 11,  # R base_u, base_v, F*_n, G*_n, P1, Q1, depth, d_x, d_y; W 2 RHS
+    "solve2": 8 * 12,
     "final": 8 * 7,     # R w*, bed_eff, P2, Q2; W w, P, Q
     "ghost_t": 0, "ghost_n": 0,
 }

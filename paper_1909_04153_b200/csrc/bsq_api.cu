@@ -38,7 +38,7 @@ enum Arr {
     A_W0, A_P0, A_Q0, A_W1, A_P1, A_Q1,
     A_BE, A_DEP, A_DDX, A_DDY, A_BFX, A_BFY,
     A_AX, A_DENX, A_RDENX, A_CWX, A_AY, A_DENY, A_RDENY, A_CWY,
-    A_BU, A_BV, A_US, A_VS, A_P2, A_Q2, A_SCRX, A_SCRY,
+    A_BU, A_BV, A_US, A_VS, A_P2, A_Q2,
     A_HIST0,  // 4 slots x 5 fields follow
     A_COUNT = A_HIST0 + 20
 };
@@ -486,12 +486,13 @@ static StagePtrs<double> stage_ptrs(bsq_ctx *c, int slot) {
     return A;
 }
 
-static SolvePtrs<double> solve_ptrs(bsq_ctx *c, int phase, int slot, int nxt_state) {
+// phase 1 solves U*, V* into the pending state's P, Q; phase 2 solves the
+// corrected right-hand sides (written over us / vs) into P2, Q2.
+static SolvePtrs<double> solve_ptrs(bsq_ctx *c, int phase, int nxt_state) {
     SolvePtrs<double> S;
     memset(&S, 0, sizeof(S));
-    S.dep = c->arr[A_DEP];
-    S.ddx = c->arr[A_DDX];
-    S.ddy = c->arr[A_DDY];
+    S.rx = c->arr[A_US];
+    S.ry = c->arr[A_VS];
     S.gp = c->Pp(nxt_state);
     S.gq = c->Qq(nxt_state);
     S.ax = c->arr[A_AX];
@@ -504,24 +505,30 @@ static SolvePtrs<double> solve_ptrs(bsq_ctx *c, int phase, int slot, int nxt_sta
     S.rdeny = c->arr[A_RDENY];
     S.cwy = c->arr[A_CWY];
     S.cy_last = c->cy_last;
-    S.scrx = c->arr[A_SCRX];
-    S.scry = c->arr[A_SCRY];
     if (phase == 1) {
-        S.rx = c->arr[A_US];
-        S.ry = c->arr[A_VS];
         S.outx = c->Pp(nxt_state);
         S.outy = c->Qq(nxt_state);
     } else {
-        S.rx = c->arr[A_BU];
-        S.ry = c->arr[A_BV];
-        S.fs = c->H(slot, 3);
-        S.gs = c->H(slot, 4);
-        S.q1 = c->Qq(nxt_state);
-        S.p1 = c->Pp(nxt_state);
         S.outx = c->arr[A_P2];
         S.outy = c->arr[A_Q2];
     }
     return S;
+}
+
+static CorrectPtrs<double> correct_ptrs(bsq_ctx *c, int slot, int nxt_state) {
+    CorrectPtrs<double> K;
+    K.bu = c->arr[A_BU];
+    K.bv = c->arr[A_BV];
+    K.fs = c->H(slot, 3);
+    K.gs = c->H(slot, 4);
+    K.p1 = c->Pp(nxt_state);
+    K.q1 = c->Qq(nxt_state);
+    K.dep = c->arr[A_DEP];
+    K.ddx = c->arr[A_DDX];
+    K.ddy = c->arr[A_DDY];
+    K.us = c->arr[A_US];
+    K.vs = c->arr[A_VS];
+    return K;
 }
 
 static void fill_result(bsq_ctx *c, bsq_step_result *r) {
@@ -554,10 +561,12 @@ int bsq_step(bsq_ctx *c, const bsq_step_params *p, bsq_step_result *r) {
     launch_ghost(c->C, c->dparams, 1, c->W(nxt), c->Pp(cur), c->Qq(cur), c->W(nxt), c->Pp(nxt),
                  c->Qq(nxt), c->st);
     ev_mark(c, "ghost_n");
-    launch_solve(c->C, solve_ptrs(c, 1, slot, nxt), 1, c->st);
+    launch_solve(c->C, solve_ptrs(c, 1, nxt), c->st);
     ev_mark(c, "solve1");
     if (c->d.cross_correction) {
-        launch_solve(c->C, solve_ptrs(c, 2, slot, nxt), 2, c->st);
+        launch_correct(c->C, correct_ptrs(c, slot, nxt), c->st);
+        ev_mark(c, "correct");
+        launch_solve(c->C, solve_ptrs(c, 2, nxt), c->st);
         ev_mark(c, "solve2");
     }
     FinalPtrs<double> F;
@@ -633,10 +642,8 @@ int bsq_solve_momentum(bsq_ctx *c, const double *us, const double *vs, const dou
                        cudaMemcpyHostToDevice, c->st));
     CU(cudaMemcpyAsync(c->Qq(nxt) + L.at(ny + GL, GL), qgn, sizeof(double) * nx,
                        cudaMemcpyHostToDevice, c->st));
-    SolvePtrs<double> S = solve_ptrs(c, 1, 0, nxt);
-    S.outx = c->arr[A_P2];
-    S.outy = c->arr[A_Q2];
-    launch_solve(c->C, S, 1, c->st);
+    SolvePtrs<double> S = solve_ptrs(c, 2, nxt);  // into P2 / Q2
+    launch_solve(c->C, S, c->st);
     CU(cudaGetLastError());
     if ((rc = download_interior(c, pout, c->arr[A_P2])) ||
         (rc = download_interior(c, qout, c->arr[A_Q2])))
@@ -702,7 +709,7 @@ int bsq_kernel_times(bsq_ctx *c, int max_n, float *ms, const char **names, int *
 
 int bsq_kernels_per_step(bsq_ctx *c) {
     if (!c) return 0;
-    return c->d.cross_correction ? 6 : 5;
+    return c->d.cross_correction ? 7 : 5;
 }
 
 }  // extern "C"

@@ -1,0 +1,216 @@
+// bsq_final.cu -- the post-solve pass of a step and the CFL reductions.
+//
+// Per interior cell, in the reference's order (stepper.py:281-305):
+// clamp w >= bed_eff with the clamped-volume tally, install the solved
+// momenta, film cutoff, sponge bands N, S, E, W (boundary.py:264-300), then
+// the blow-up deviation, non-finite scan and speed extrema
+// (_kernels.py:324-353) of the final state.  Reductions: registers -> warp
+// shuffles -> CTA -> per-CTA partials -> the last CTA to finish reduces the
+// partials in a fixed order, so results are run-to-run deterministic (max is
+// order free; the clamped-volume sum has a fixed association).
+#include <cmath>
+#include <cstdint>
+
+#include "bsq_device.cuh"
+#include "bsq_launch.h"
+
+namespace bsq {
+
+constexpr int FX = 32, FY = 8, FR = 4;  // block 32 x 8 threads, 4 rows per thread
+constexpr int FT = FX * FY, FWARPS = FT / 32;
+
+struct Red {
+    double rate, speed, depth, dev, clamp;
+    int nan;
+};
+
+__device__ __forceinline__ void red_warp(Red &r) {
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) {
+        r.rate = fmax(r.rate, __shfl_xor_sync(0xffffffffu, r.rate, m));
+        r.speed = fmax(r.speed, __shfl_xor_sync(0xffffffffu, r.speed, m));
+        r.depth = fmax(r.depth, __shfl_xor_sync(0xffffffffu, r.depth, m));
+        r.dev = fmax(r.dev, __shfl_xor_sync(0xffffffffu, r.dev, m));
+        r.clamp = r.clamp + __shfl_xor_sync(0xffffffffu, r.clamp, m);
+        r.nan |= __shfl_xor_sync(0xffffffffu, r.nan, m);
+    }
+}
+
+// CTA-wide reduction; result valid in thread 0
+__device__ __forceinline__ Red red_block(Red r) {
+    __shared__ Red s[FWARPS];
+    const int tid = threadIdx.y * FX + threadIdx.x;
+    red_warp(r);
+    __syncthreads();  // protect s against a previous use
+    if ((tid & 31) == 0) s[tid >> 5] = r;
+    __syncthreads();
+    if (tid == 0) {
+        Red t = s[0];
+        for (int k = 1; k < FWARPS; k++) {
+            t.rate = fmax(t.rate, s[k].rate);
+            t.speed = fmax(t.speed, s[k].speed);
+            t.depth = fmax(t.depth, s[k].depth);
+            t.dev = fmax(t.dev, s[k].dev);
+            t.clamp = t.clamp + s[k].clamp;
+            t.nan |= s[k].nan;
+        }
+        r = t;
+    }
+    return r;
+}
+
+// speed_extrema contribution of one cell (_kernels.py:337-352); the serial
+// scan's `if x > max` skips NaN, hence the !(x > 0) guards.
+template <class T>
+__device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, T be, Red &r) {
+    T h = w - be;
+    if (h < T(0)) h = T(0);
+    const T hstar = h > C.h_eps ? h : C.h_eps;
+    const T c = sqrt(C.g * h);
+    const T su = fabs(p) / hstar + c;
+    const T sv = fabs(q) / hstar + c;
+    const double rate = double(nb_max(su * C.inv_dx, sv * C.inv_dy));
+    const double speed = double(nb_max(su, sv));
+    if (rate > r.rate) r.rate = rate;
+    if (speed > r.speed) r.speed = speed;
+    if (double(h) > r.depth) r.depth = double(h);
+}
+
+template <class T>
+__global__ void __launch_bounds__(FT) k_final(Consts<T> C, FinalPtrs<T> F) {
+    __shared__ bool am_last;
+    const Layout L = C.L;
+    const int nx = L.nx, ny = L.ny;
+    const int I = GL + blockIdx.x * FX + threadIdx.x;
+    Red r{0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < FR; k++) {
+        const int J = GL + (blockIdx.y * FR + k) * FY + threadIdx.y;
+        if (I >= nx + GL || J >= ny + GL) continue;
+        const long o = L.at(J, I);
+        const T be = F.be[o];
+        T w = F.w[o];
+        T p = F.pin[o], q = F.qin[o];
+        // clamp and volume tally (stepper.py:281-285); np.maximum keeps NaN
+        const T def = be - w;
+        if (def > T(0) || def != def) r.clamp = r.clamp + double(def);
+        w = (w >= be || w != w) ? w : be;
+        // film cutoff (stepper.py:288-292)
+        if (C.h_dry > T(0) && (w - be) < C.h_dry) {
+            p = T(0);
+            q = T(0);
+        }
+        const T rest = C.ws > be ? C.ws : be;  // np.maximum(ws, bed_eff)
+#pragma unroll
+        for (int side = 0; side < 4; side++) {  // sponge bands, order N, S, E, W
+            if (C.side_kind[side] != KIND_SPONGE || C.sponge_len[side] == 0) continue;
+            const int kk = (side == SIDE_E || side == SIDE_W) ? (I - GL) - C.sponge_lo[side]
+                                                              : (J - GL) - C.sponge_lo[side];
+            if (kk < 0 || kk >= C.sponge_len[side]) continue;
+            const T fac = F.fac[side][kk];
+            w = rest + (w - rest) * fac;
+            p = p * fac;
+            q = q * fac;
+        }
+        F.w[o] = w;
+        F.pout[o] = p;
+        F.qout[o] = q;
+        T dv = w - rest;  // blow-up deviation (stepper.py:295)
+        dv = dv < T(0) ? -dv : dv;
+        if (dv != dv) r.nan = 1;
+        else if (double(dv) > r.dev) r.dev = double(dv);
+        const unsigned long long lin = (unsigned long long)(J - GL) * nx + (I - GL);
+        if (!isfinite(w)) atomicMin(&F.res->state_bad[0], lin);
+        if (!isfinite(p)) atomicMin(&F.res->state_bad[1], lin);
+        if (!isfinite(q)) atomicMin(&F.res->state_bad[2], lin);
+        extrema_cell(C, w, p, q, be, r);
+    }
+    r = red_block(r);
+    const int tid = threadIdx.y * FX + threadIdx.x;
+    const int nblk = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
+    if (tid == 0) {
+        Partial pt;
+        pt.max_rate = r.rate;
+        pt.max_speed = r.speed;
+        pt.max_depth = r.depth;
+        pt.max_dev = r.dev;
+        pt.clamped = r.clamp;
+        pt.dev_nan = r.nan;
+        pt.pad_ = 0;
+        F.part[bid] = pt;
+        __threadfence();
+        const unsigned int prev = atomicAdd(F.counter, 1u);
+        am_last = prev == (unsigned int)(nblk - 1);
+    }
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    // last CTA: reduce the partials; thread t folds partials t, t+FT, ... in order
+    Red a{0, 0, 0, 0, 0, 0};
+    for (int k = tid; k < nblk; k += FT) {
+        const volatile Partial *pp = (const volatile Partial *)&F.part[k];
+        a.rate = fmax(a.rate, pp->max_rate);
+        a.speed = fmax(a.speed, pp->max_speed);
+        a.depth = fmax(a.depth, pp->max_depth);
+        a.dev = fmax(a.dev, pp->max_dev);
+        a.clamp = a.clamp + pp->clamped;
+        a.nan |= pp->dev_nan;
+    }
+    a = red_block(a);
+    if (tid == 0) {
+        F.res->max_rate = a.rate;
+        F.res->max_speed = a.speed;
+        F.res->max_depth = a.depth;
+        F.res->max_dev = a.nan ? (double)NAN : a.dev;
+        F.res->clamped = a.clamp;
+        *F.counter = 0u;
+    }
+}
+
+// speed_extrema of a committed state (construction time, stepper.py:210)
+template <class T>
+__global__ void __launch_bounds__(FT) k_extrema(Consts<T> C, const T *w, const T *p, const T *q,
+                                                const T *be, Partial *part) {
+    const Layout L = C.L;
+    const int I = GL + blockIdx.x * FX + threadIdx.x;
+    Red r{0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < FR; k++) {
+        const int J = GL + (blockIdx.y * FR + k) * FY + threadIdx.y;
+        if (I >= L.nx + GL || J >= L.ny + GL) continue;
+        const long o = L.at(J, I);
+        extrema_cell(C, w[o], p[o], q[o], be[o], r);
+    }
+    r = red_block(r);
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        Partial pt{};
+        pt.max_rate = r.rate;
+        pt.max_speed = r.speed;
+        pt.max_depth = r.depth;
+        part[blockIdx.y * gridDim.x + blockIdx.x] = pt;
+    }
+}
+
+static dim3 final_grid(int nx, int ny) { return dim3((nx + FX - 1) / FX, (ny + FY * FR - 1) / (FY * FR)); }
+
+int final_blocks(int nx, int ny) {
+    dim3 g = final_grid(nx, ny);
+    return (int)(g.x * g.y);
+}
+
+template <class T>
+void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st) {
+    k_final<T><<<final_grid(C.L.nx, C.L.ny), dim3(FX, FY), 0, st>>>(C, F);
+}
+
+template <class T>
+void launch_extrema(const Consts<T> &C, const T *w, const T *p, const T *q, const T *be,
+                    Partial *part, cudaStream_t st) {
+    k_extrema<T><<<final_grid(C.L.nx, C.L.ny), dim3(FX, FY), 0, st>>>(C, w, p, q, be, part);
+}
+
+template void launch_final<double>(const Consts<double> &, const FinalPtrs<double> &,
+                                   cudaStream_t);
+template void launch_extrema<double>(const Consts<double> &, const double *, const double *,
+                                     const double *, const double *, Partial *, cudaStream_t);
+
+}  // namespace bsq

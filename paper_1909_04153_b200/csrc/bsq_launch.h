@@ -20,15 +20,19 @@ struct StagePtrs {
 
 template <class T>
 struct SolvePtrs {
-    const T *rx, *ry;               // phase 1: us, vs;  phase 2: base_u, base_v
-    const T *fs, *gs;               // phase 2: stored F*_n, G*_n
-    const T *q1, *p1;               // phase 2: first-solve Q (for F*) and P (for G*)
+    const T *rx, *ry;               // folded-later right-hand sides (U*, V* or corrected)
+    const T *gp, *gq;               // arrays holding the P / Q ghost values to fold
+    const T *ax, *denx, *rdenx, *cwx, *cx_last;  // x-line LU factors
+    const T *ay, *deny, *rdeny, *cwy, *cy_last;  // y-line LU factors
+    T *outx, *outy;                 // solved P (rows) and Q (columns); also dw scratch
+};
+
+template <class T>
+struct CorrectPtrs {
+    const T *bu, *bv, *fs, *gs;     // quadrature bases and stored F*_n, G*_n
+    const T *p1, *q1;               // first-solve momenta with ghosts
     const T *dep, *ddx, *ddy;
-    const T *gp, *gq;               // arrays holding the P / Q ghost values used for folding
-    const T *ax, *denx, *rdenx, *cwx, *cx_last;
-    const T *ay, *deny, *rdeny, *cwy, *cy_last;
-    T *scrx, *scry;                 // forward-sweep scratch
-    T *outx, *outy;                 // solved P (rows) and Q (columns)
+    T *us, *vs;                     // corrected right-hand sides
 };
 
 template <class T>
@@ -50,7 +54,9 @@ template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
                   cudaStream_t st);
 template <class T>
-void launch_solve(const Consts<T> &C, const SolvePtrs<T> &S, int phase, cudaStream_t st);
+void launch_solve(const Consts<T> &C, const SolvePtrs<T> &S, cudaStream_t st);
+template <class T>
+void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st);
 template <class T>
 void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st);
 template <class T>
