@@ -1,0 +1,98 @@
+// bsq_ghost.cu -- ghost-strip fill (boundary policies) for the Boussinesq step.
+//
+// A step launches, in order (see DESIGN.md for the HBM budget of each):
+//   k_ghost      ghost strips at t                       (boundary.py:316-323)
+//   k_stage      fused stage set + predictor             (bsq_stage.cu)
+//   k_ghost      strips of the predicted state at t+dt   (stepper.py:252-254)
+//   k_solve_pipe first x/y line solves                   (bsq_solve.cu)
+//   k_correct    cross-correction right-hand sides       (bsq_solve.cu)
+//   k_solve_pipe second x/y line solves
+//   k_final      clamp, film, sponge, checks, extrema    (bsq_final.cu)
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "bsq_device.cuh"
+#include "bsq_launch.h"
+
+namespace bsq {
+
+// ---------------------------------------------------------------------------
+// ghost strips
+
+template <class T>
+__device__ __forceinline__ T ns_value(const Consts<T> &C, const DevParams *P, int which, int f,
+                                      int J, int I, const T *src) {
+    // value the N or S fill writes at ghost row J, column I (boundary.py:206-261)
+    const int nyt = C.L.ny + 4;
+    const int side = J < GL ? SIDE_S : SIDE_N;
+    if (C.side_kind[side] == KIND_MAKER) {
+        double gw = which ? P->gw_n[side] : P->gw_t[side];
+        double gf = which ? P->gf_n[side] : P->gf_t[side];
+        if (f == 0) return T(gw);
+        if (f == 1) return T(0);
+        return side == SIDE_S ? T(gf) : T(-gf);
+    }
+    int Jm = side == SIDE_S ? (J == GL - 1 ? GL : GL + 1) : (J == nyt - GL ? nyt - GL - 1 : nyt - GL - 2);
+    T s = f == 2 ? T(-1) : T(1);
+    return s * src[C.L.at(Jm, I)];
+}
+
+// One thread per ghost cell.  Threads [0, 4*nyt) cover the E/W strips over
+// all rows (they own the corners: fill order N, S, E, W); threads
+// [4*nyt, 4*nyt + 4*nx) the N/S strips over interior columns.  Corner values
+// compose the N/S rule at the mirror column, so no ordering between threads
+// is needed.  src_w/src_p/src_q give the interior the mirrors read (for the
+// t+dt fill: predicted w, old P/Q -- stepper.py:252-254).
+template <class T>
+__global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which, const T *src_w,
+                        const T *src_p, const T *src_q, T *dst_w, T *dst_p, T *dst_q) {
+    const int nx = C.L.nx, ny = C.L.ny, nxt = nx + 4, nyt = ny + 4;
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const T *src[3] = {src_w, src_p, src_q};
+    T *dst[3] = {dst_w, dst_p, dst_q};
+    if (k < 4 * nyt) {
+        int J = k >> 2;
+        int c = k & 3;  // 0,1 -> west cols 0,1; 2,3 -> east cols nxt-2, nxt-1
+        int I = c < 2 ? c : nxt - 4 + c;
+        int side = c < 2 ? SIDE_W : SIDE_E;
+        bool interior_row = J >= GL && J < nyt - GL;
+        if (C.side_kind[side] == KIND_MAKER) {
+            double gw = which ? P->gw_n[side] : P->gw_t[side];
+            double gf = which ? P->gf_n[side] : P->gf_t[side];
+            dst_w[C.L.at(J, I)] = T(gw);
+            dst_p[C.L.at(J, I)] = side == SIDE_W ? T(gf) : T(-gf);
+            dst_q[C.L.at(J, I)] = T(0);
+            return;
+        }
+        int Im = side == SIDE_W ? (I == GL - 1 ? GL : GL + 1) : (I == nxt - GL ? nxt - GL - 1 : nxt - GL - 2);
+#pragma unroll
+        for (int f = 0; f < 3; f++) {
+            T cur = interior_row ? src[f][C.L.at(J, Im)] : ns_value(C, P, which, f, J, Im, src[f]);
+            T s = f == 1 ? T(-1) : T(1);  // P is the wall-normal flux on E/W
+            dst[f][C.L.at(J, I)] = s * cur;
+        }
+        return;
+    }
+    k -= 4 * nyt;
+    if (k < 4 * nx) {
+        int I = GL + (k >> 2);
+        int r = k & 3;
+        int J = r < 2 ? r : nyt - 4 + r;
+#pragma unroll
+        for (int f = 0; f < 3; f++) dst[f][C.L.at(J, I)] = ns_value(C, P, which, f, J, I, src[f]);
+    }
+}
+
+template <class T>
+void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
+                  const T *sq, T *dw, T *dp, T *dq, cudaStream_t st) {
+    int n = 4 * (C.L.ny + 4) + 4 * C.L.nx;
+    k_ghost<T><<<(n + 127) / 128, 128, 0, st>>>(C, P, which, sw, sp, sq, dw, dp, dq);
+}
+
+template void launch_ghost<double>(const Consts<double> &, const DevParams *, int, const double *,
+                                   const double *, const double *, double *, double *, double *,
+                                   cudaStream_t);
+
+}  // namespace bsq

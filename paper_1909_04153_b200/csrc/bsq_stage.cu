@@ -1,20 +1,24 @@
-// bsq_kernels.cu -- sm_100a kernels of one adaptive-AB3 Boussinesq step.
+// bsq_stage.cu -- the fused stage kernel: everything a step evaluates on the
+// state at t_n, in one pass over HBM.
 //
-// One step (stepper.py:225-305) is five device passes over the pitched
-// fields (see DESIGN.md for the HBM budget of each):
+// Per interior cell this computes the reference's
+//   faces_x/faces_y  (_kernels.py:29-103)   limited faces + positivity shift
+//   flux_x/flux_y    (_kernels.py:106-212)  central-upwind fluxes, wet/dry
+//   fv_rates         (_kernels.py:215-251)  divergence, bed source, friction
+//   eta + dispersive_rates (dispersion.py:87, _kernels.py:254-288)
+//   cross_rates      (_kernels.py:291-321)  F*, G*
+//   compute_ustar_vstar (dispersion.py:120-149)
+//   Euler / AB3 predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
+// and writes the new stage level, the predicted w, U*, V* and the
+// quadrature bases.  Faces and fluxes live only in shared memory.
 //
-//   k_ghost   ghost strips at t          (boundary.py:316-323)
-//   k_stage   faces + central-upwind fluxes + FV rates + dispersive terms +
-//             cross groups + U*/V* + Euler/AB3/VFD predictor, one fused
-//             smem-tiled stencil pass (dispersion.py:67-149, stepper.py:109-132)
-//   k_ghost   ghost strips of the predicted state at t+dt (stepper.py:252-254)
-//   k_solve   x-line (P) and y-line (Q) tridiagonal solves, pre-factored
-//             Thomas (implicit.py:173-205, _kernels.py:360-381); phase 2 folds
-//             the cross-correction RHS (stepper.py:262-280) into its loads
-//   k_final   clamp + film cutoff + sponge + blow-up/non-finite scan + CFL
-//             extrema, with a deterministic last-block reduction
-//             (stepper.py:281-305, boundary.py:264-300, _kernels.py:324-353)
-#include <cfloat>
+// CTA = 32 x 8 cells.  Phases (each ends in __syncthreads):
+//   A  load w, P, Q (+ eta) for the tile and a 2-cell halo, and face beds
+//   B  faces of every cell once: x faces for columns -1..32, y faces for
+//      rows -1..8 of the tile (the reference evaluates each face once too)
+//   C  fluxes of the 33 x 8 x-interfaces and 32 x 9 y-interfaces, held in
+//      registers across a barrier and stored over the dead face buffers
+//   D  per-cell rates, dispersive terms, cross groups, U*/V*, predictor
 #include <cmath>
 #include <cstdint>
 
@@ -23,216 +27,258 @@
 
 namespace bsq {
 
-// ---------------------------------------------------------------------------
-// ghost strips
+constexpr int TX = 32, TY = 8, NT = TX * TY;
+constexpr int HX = TX + 4, HY = TY + 4;       // tile + 2-cell halo
+constexpr int FXW = TX + 2, FYH = TY + 2;     // cells with x faces per row / rows with y faces
+constexpr int NXF = TY * FXW, NYF = FYH * TX; // face items
+constexpr int NXI = TY * (TX + 1), NYI = (TY + 1) * TX;  // interface items
+constexpr int NFL = NXI + NYI;
+constexpr int FL_PASSES = (NFL + NT - 1) / NT;
 
 template <class T>
-__device__ __forceinline__ T ns_value(const Consts<T> &C, const DevParams *P, int which, int f,
-                                      int J, int I, const T *src) {
-    // value the N or S fill writes at ghost row J, column I (boundary.py:206-261)
-    const int nyt = C.L.ny + 4;
-    const int side = J < GL ? SIDE_S : SIDE_N;
-    if (C.side_kind[side] == KIND_MAKER) {
-        double gw = which ? P->gw_n[side] : P->gw_t[side];
-        double gf = which ? P->gf_n[side] : P->gf_t[side];
-        if (f == 0) return T(gw);
-        if (f == 1) return T(0);
-        return side == SIDE_S ? T(gf) : T(-gf);
-    }
-    int Jm = side == SIDE_S ? (J == GL - 1 ? GL : GL + 1) : (J == nyt - GL ? nyt - GL - 1 : nyt - GL - 2);
-    T s = f == 2 ? T(-1) : T(1);
-    return s * src[C.L.at(Jm, I)];
+struct StageSmem {
+    T w[HY][HX], p[HY][HX], q[HY][HX], eta[HY][HX];
+    T bfx[TY][TX + 3];  // bed_face_x for columns -2..TX
+    T bfy[TY + 3][TX];  // bed_face_y for rows -2..TY
+    union {
+        struct {  // phase B/C: faces (hi = east/north, lo = west/south)
+            T xwhi[TY][FXW], xwlo[TY][FXW], xphi[TY][FXW], xplo[TY][FXW], xqhi[TY][FXW],
+                xqlo[TY][FXW];
+            T ywhi[FYH][TX], ywlo[FYH][TX], yphi[FYH][TX], yplo[FYH][TX], yqhi[FYH][TX],
+                yqlo[FYH][TX];
+        } f;
+        struct {  // phase C/D: fluxes through the tile's interfaces
+            T fx[3][TY][TX + 1];
+            T fy[3][TY + 1][TX];
+        } x;
+    } u;
+};
+
+// Markstein quotient x/d from r = RN(1/d), robust to non-finite x: a
+// non-finite product returns IEEE's x/d (inf or NaN) so the non-finite
+// stage scan sees exactly the reference's cells.
+template <class T>
+__device__ __forceinline__ T div_rcp(T x, T d, T r) {
+    T q0 = x * r;
+    T e = fma_rn(-q0, d, x);
+    T q1 = fma_rn(e, r, q0);
+    return (e == T(0) || q1 != q1) ? q0 : q1;
 }
 
-// One thread per ghost cell.  Threads [0, 4*nyt) cover the E/W strips over
-// all rows (they own the corners: fill order N, S, E, W); threads
-// [4*nyt, 4*nyt + 4*nx) the N/S strips over interior columns.  Corner values
-// compose the N/S rule at the mirror column, so no ordering between threads
-// is needed.  src_w/src_p/src_q give the interior the mirrors read (for the
-// t+dt fill: predicted w, old P/Q -- stepper.py:252-254).
+__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+
+// cu_flux (bsq_device.cuh) with the two divisions by each side's depth
+// sharing one correctly rounded reciprocal: ul = nl/dl and nl*tl/dl are
+// still the correctly rounded quotients.
 template <class T>
-__global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which, const T *src_w,
-                        const T *src_p, const T *src_q, T *dst_w, T *dst_p, T *dst_q) {
-    const int nx = C.L.nx, ny = C.L.ny, nxt = nx + 4, nyt = ny + 4;
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const T *src[3] = {src_w, src_p, src_q};
-    T *dst[3] = {dst_w, dst_p, dst_q};
-    if (k < 4 * nyt) {
-        int J = k >> 2;
-        int c = k & 3;  // 0,1 -> west cols 0,1; 2,3 -> east cols nxt-2, nxt-1
-        int I = c < 2 ? c : nxt - 4 + c;
-        int side = c < 2 ? SIDE_W : SIDE_E;
-        bool interior_row = J >= GL && J < nyt - GL;
-        if (C.side_kind[side] == KIND_MAKER) {
-            double gw = which ? P->gw_n[side] : P->gw_t[side];
-            double gf = which ? P->gf_n[side] : P->gf_t[side];
-            dst_w[C.L.at(J, I)] = T(gw);
-            dst_p[C.L.at(J, I)] = side == SIDE_W ? T(gf) : T(-gf);
-            dst_q[C.L.at(J, I)] = T(0);
-            return;
-        }
-        int Im = side == SIDE_W ? (I == GL - 1 ? GL : GL + 1) : (I == nxt - GL ? nxt - GL - 1 : nxt - GL - 2);
-#pragma unroll
-        for (int f = 0; f < 3; f++) {
-            T cur = interior_row ? src[f][C.L.at(J, Im)] : ns_value(C, P, which, f, J, Im, src[f]);
-            T s = f == 1 ? T(-1) : T(1);  // P is the wall-normal flux on E/W
-            dst[f][C.L.at(J, I)] = s * cur;
-        }
+__device__ __forceinline__ void cu_flux_rcp(T wl, T wr, T nl_, T nr_, T tl_, T tr_, T bf, T g,
+                                            T h_eps, T &f_mass, T &f_norm, T &f_tang) {
+    T hl = wl - bf;
+    if (hl < T(0)) hl = T(0);
+    T hr = wr - bf;
+    if (hr < T(0)) hr = T(0);
+    const T nl = hl > T(0) ? nl_ : T(0), tl = hl > T(0) ? tl_ : T(0);
+    const T nr = hr > T(0) ? nr_ : T(0), tr = hr > T(0) ? tr_ : T(0);
+    const T dl = hl > h_eps ? hl : h_eps;
+    const T dr = hr > h_eps ? hr : h_eps;
+    const T rl = rcp_rn(dl), rr = rcp_rn(dr);
+    const T ul = div_rcp(nl, dl, rl);
+    const T ur = div_rcp(nr, dr, rr);
+    const T cl = sqrt(g * hl);
+    const T cr = sqrt(g * hr);
+    const T ap = nb_max(nb_max(ul + cl, ur + cr), T(0));
+    const T am = nb_min(nb_min(ul - cl, ur - cr), T(0));
+    if (ap == T(0) && am == T(0)) {
+        f_mass = T(0);
+        f_norm = T(0);
+        f_tang = T(0);
         return;
     }
-    k -= 4 * nyt;
-    if (k < 4 * nx) {
-        int I = GL + (k >> 2);
-        int r = k & 3;
-        int J = r < 2 ? r : nyt - 4 + r;
-#pragma unroll
-        for (int f = 0; f < 3; f++) dst[f][C.L.at(J, I)] = ns_value(C, P, which, f, J, I, src[f]);
-    }
+    const T inv = rcp_rn(ap - am);
+    const T diff = ap * am * inv;
+    const T fnl = nl * ul + T(0.5) * g * hl * hl;
+    const T fnr = nr * ur + T(0.5) * g * hr * hr;
+    const T ftl = div_rcp(nl * tl, dl, rl);
+    const T ftr = div_rcp(nr * tr, dr, rr);
+    f_mass = (ap * nl - am * nr) * inv + diff * (wr - wl);
+    f_norm = (ap * fnl - am * fnr) * inv + diff * (nr - nl);
+    f_tang = (ap * ftl - am * ftr) * inv + diff * (tr - tl);
 }
 
-// ---------------------------------------------------------------------------
-// fused stage + predictor
-
-constexpr int TX = 32, TY = 8;
-constexpr int HX = TX + 4, HY = TY + 4;
-
 template <class T>
-__global__ void __launch_bounds__(TX *TY) k_stage(Consts<T> C, const DevParams *__restrict__ P,
-                                                  StagePtrs<T> A, int predict) {
-    __shared__ T s_w[HY][HX], s_p[HY][HX], s_q[HY][HX], s_eta[HY][HX];
-    __shared__ T s_bfx[TY][TX + 3], s_bfy[TY + 3][TX];
-    __shared__ T s_fx[3][TY][TX + 1], s_fy[3][TY + 1][TX];
-
+__global__ void __launch_bounds__(NT, 4) k_stage(Consts<T> C, const DevParams *__restrict__ P,
+                                                 StagePtrs<T> A, int predict) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    StageSmem<T> &S = *reinterpret_cast<StageSmem<T> *>(smem_raw);
     const Layout L = C.L;
     const int nx = L.nx, ny = L.ny, nxt = nx + 4, nyt = ny + 4;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int I0 = GL + blockIdx.x * TX, J0 = GL + blockIdx.y * TY;
 
-    // tile + 2-cell halo of w, P, Q and eta = (w - bed_eff) - depth (dispersion.py:87)
-    for (int k = tid; k < HY * HX; k += TX * TY) {
-        int y = k / HX, x = k - y * HX;
-        int J = J0 - 2 + y, I = I0 - 2 + x;
+    // ---- A: tile + halo ------------------------------------------------------
+    for (int k = tid; k < HY * HX; k += NT) {
+        const int y = k / HX, x = k - y * HX;
+        const int J = J0 - 2 + y, I = I0 - 2 + x;
         T w = 0, p = 0, q = 0, e = 0;
         if (J < nyt && I < nxt) {
-            long o = L.at(J, I);
+            const long o = L.at(J, I);
             w = A.w[o];
             p = A.p[o];
             q = A.q[o];
-            e = (w - A.be[o]) - A.dep[o];
+            e = (w - A.be[o]) - A.dep[o];  // dispersion.py:87
         }
-        s_w[y][x] = w;
-        s_p[y][x] = p;
-        s_q[y][x] = q;
-        s_eta[y][x] = e;
+        S.w[y][x] = w;
+        S.p[y][x] = p;
+        S.q[y][x] = q;
+        S.eta[y][x] = e;
     }
-    for (int k = tid; k < TY * (TX + 3); k += TX * TY) {
-        int y = k / (TX + 3), x = k - y * (TX + 3);
-        int J = J0 + y, I = I0 - 2 + x;
-        s_bfx[y][x] = (J < nyt && I <= nx + 2) ? A.bfx[L.at(J, I)] : T(0);
+    for (int k = tid; k < TY * (TX + 3); k += NT) {
+        const int y = k / (TX + 3), x = k - y * (TX + 3);
+        const int J = J0 + y, I = I0 - 2 + x;
+        S.bfx[y][x] = (J < nyt && I <= nx + 2) ? A.bfx[L.at(J, I)] : T(0);
     }
-    for (int k = tid; k < (TY + 3) * TX; k += TX * TY) {
-        int y = k / TX, x = k - y * TX;
-        int J = J0 - 2 + y, I = I0 + x;
-        s_bfy[y][x] = (J <= ny + 2 && I < nxt) ? A.bfy[L.at(J, I)] : T(0);
-    }
-    __syncthreads();
-
-    // x interfaces: between smem columns xi+1 (left cell) and xi+2 (right)
-    for (int k = tid; k < TY * (TX + 1); k += TX * TY) {
-        int r = k / (TX + 1), xi = k - r * (TX + 1);
-        int y = r + 2;
-        Faces<T> fl = cell_faces(s_w[y][xi], s_w[y][xi + 1], s_w[y][xi + 2], s_p[y][xi],
-                                 s_p[y][xi + 1], s_p[y][xi + 2], s_q[y][xi], s_q[y][xi + 1],
-                                 s_q[y][xi + 2], s_bfx[r][xi + 1], s_bfx[r][xi], C.theta);
-        Faces<T> fr = cell_faces(s_w[y][xi + 1], s_w[y][xi + 2], s_w[y][xi + 3], s_p[y][xi + 1],
-                                 s_p[y][xi + 2], s_p[y][xi + 3], s_q[y][xi + 1], s_q[y][xi + 2],
-                                 s_q[y][xi + 3], s_bfx[r][xi + 2], s_bfx[r][xi + 1], C.theta);
-        T f1, f2, f3;
-        cu_flux(fl.whi, fr.wlo, fl.phi, fr.plo, fl.qhi, fr.qlo, s_bfx[r][xi + 1], C.g, C.h_eps,
-                f1, f2, f3);
-        s_fx[0][r][xi] = f1;
-        s_fx[1][r][xi] = f2;
-        s_fx[2][r][xi] = f3;
-    }
-    // y interfaces: between smem rows yi+1 (south cell) and yi+2 (north)
-    for (int k = tid; k < (TY + 1) * TX; k += TX * TY) {
-        int yi = k / TX, c = k - yi * TX;
-        int x = c + 2;
-        Faces<T> fs = cell_faces(s_w[yi][x], s_w[yi + 1][x], s_w[yi + 2][x], s_p[yi][x],
-                                 s_p[yi + 1][x], s_p[yi + 2][x], s_q[yi][x], s_q[yi + 1][x],
-                                 s_q[yi + 2][x], s_bfy[yi + 1][c], s_bfy[yi][c], C.theta);
-        Faces<T> fn = cell_faces(s_w[yi + 1][x], s_w[yi + 2][x], s_w[yi + 3][x], s_p[yi + 1][x],
-                                 s_p[yi + 2][x], s_p[yi + 3][x], s_q[yi + 1][x], s_q[yi + 2][x],
-                                 s_q[yi + 3][x], s_bfy[yi + 2][c], s_bfy[yi + 1][c], C.theta);
-        T f1, fq, fp;
-        // normal momentum is Q, tangential is P: fy2 = P flux, fy3 = Q flux
-        cu_flux(fs.whi, fn.wlo, fs.qhi, fn.qlo, fs.phi, fn.plo, s_bfy[yi + 1][c], C.g, C.h_eps,
-                f1, fq, fp);
-        s_fy[0][yi][c] = f1;
-        s_fy[1][yi][c] = fp;
-        s_fy[2][yi][c] = fq;
+    for (int k = tid; k < (TY + 3) * TX; k += NT) {
+        const int y = k / TX, x = k - y * TX;
+        const int J = J0 - 2 + y, I = I0 + x;
+        S.bfy[y][x] = (J <= ny + 2 && I < nxt) ? A.bfy[L.at(J, I)] : T(0);
     }
     __syncthreads();
 
+    // ---- B: faces, once per cell ------------------------------------------------
+    for (int k = tid; k < NXF + NYF; k += NT) {
+        if (k < NXF) {  // x faces of cell (row r, column c-1), c = 0..TX+1
+            const int r = k / FXW, c = k - r * FXW;
+            const int y = r + 2, x = c + 1;  // smem coords of the cell
+            const Faces<T> f = cell_faces(S.w[y][x - 1], S.w[y][x], S.w[y][x + 1], S.p[y][x - 1],
+                                          S.p[y][x], S.p[y][x + 1], S.q[y][x - 1], S.q[y][x],
+                                          S.q[y][x + 1], S.bfx[r][c + 1], S.bfx[r][c], C.theta);
+            S.u.f.xwhi[r][c] = f.whi;
+            S.u.f.xwlo[r][c] = f.wlo;
+            S.u.f.xphi[r][c] = f.phi;
+            S.u.f.xplo[r][c] = f.plo;
+            S.u.f.xqhi[r][c] = f.qhi;
+            S.u.f.xqlo[r][c] = f.qlo;
+        } else {  // y faces of cell (row r-1, column c), r = 0..TY+1
+            const int kk = k - NXF;
+            const int r = kk / TX, c = kk - r * TX;
+            const int y = r + 1, x = c + 2;
+            const Faces<T> f = cell_faces(S.w[y - 1][x], S.w[y][x], S.w[y + 1][x], S.p[y - 1][x],
+                                          S.p[y][x], S.p[y + 1][x], S.q[y - 1][x], S.q[y][x],
+                                          S.q[y + 1][x], S.bfy[r + 1][c], S.bfy[r][c], C.theta);
+            S.u.f.ywhi[r][c] = f.whi;
+            S.u.f.ywlo[r][c] = f.wlo;
+            S.u.f.yphi[r][c] = f.phi;
+            S.u.f.yplo[r][c] = f.plo;
+            S.u.f.yqhi[r][c] = f.qhi;
+            S.u.f.yqlo[r][c] = f.qlo;
+        }
+    }
+    __syncthreads();
+
+    // ---- C: fluxes (registers across the barrier, then over the faces) ----------
+    T fl[FL_PASSES][3];
+#pragma unroll
+    for (int s = 0; s < FL_PASSES; s++) {
+        const int k = tid + s * NT;
+        if (k < NXI) {  // interface between tile columns xi-1 and xi, row r
+            const int r = k / (TX + 1), xi = k - r * (TX + 1);
+            // left cell = face column xi, right cell = face column xi+1
+            cu_flux_rcp(S.u.f.xwhi[r][xi], S.u.f.xwlo[r][xi + 1], S.u.f.xphi[r][xi],
+                        S.u.f.xplo[r][xi + 1], S.u.f.xqhi[r][xi], S.u.f.xqlo[r][xi + 1],
+                        S.bfx[r][xi + 1], C.g, C.h_eps, fl[s][0], fl[s][1], fl[s][2]);
+        } else if (k < NFL) {  // interface between tile rows yi-1 and yi, column c
+            const int kk = k - NXI;
+            const int yi = kk / TX, c = kk - yi * TX;
+            // south cell = face row yi, north cell = face row yi+1; normal = Q
+            T f1, fq, fp;
+            cu_flux_rcp(S.u.f.ywhi[yi][c], S.u.f.ywlo[yi + 1][c], S.u.f.yqhi[yi][c],
+                        S.u.f.yqlo[yi + 1][c], S.u.f.yphi[yi][c], S.u.f.yplo[yi + 1][c],
+                        S.bfy[yi + 1][c], C.g, C.h_eps, f1, fq, fp);
+            fl[s][0] = f1;
+            fl[s][1] = fp;  // fy2 carries P
+            fl[s][2] = fq;  // fy3 carries Q
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < FL_PASSES; s++) {
+        const int k = tid + s * NT;
+        if (k < NXI) {
+            const int r = k / (TX + 1), xi = k - r * (TX + 1);
+            S.u.x.fx[0][r][xi] = fl[s][0];
+            S.u.x.fx[1][r][xi] = fl[s][1];
+            S.u.x.fx[2][r][xi] = fl[s][2];
+        } else if (k < NFL) {
+            const int kk = k - NXI;
+            const int yi = kk / TX, c = kk - yi * TX;
+            S.u.x.fy[0][yi][c] = fl[s][0];
+            S.u.x.fy[1][yi][c] = fl[s][1];
+            S.u.x.fy[2][yi][c] = fl[s][2];
+        }
+    }
+    __syncthreads();
+
+    // ---- D: per cell ----------------------------------------------------------------
     const int J = J0 + ty, I = I0 + tx;
     if (J >= ny + GL || I >= nx + GL) return;
     const int y = ty + 2, x = tx + 2;
     const long o = L.at(J, I);
-    const T wc = s_w[y][x], pc = s_p[y][x], qc = s_q[y][x];
+    const T wc = S.w[y][x], pc = S.p[y][x], qc = S.q[y][x];
+    const T be_ = S.bfx[ty][tx + 2], bw_ = S.bfx[ty][tx + 1];
+    const T bn_ = S.bfy[ty + 2][tx], bs_ = S.bfy[ty + 1][tx];
 
-    // fv_rates (_kernels.py:226-251)
-    T rw = -(s_fx[0][ty][tx + 1] - s_fx[0][ty][tx]) * C.inv_dx -
-           (s_fy[0][ty + 1][tx] - s_fy[0][ty][tx]) * C.inv_dy;
-    T be_ = s_bfx[ty][tx + 2], bw_ = s_bfx[ty][tx + 1];
-    T bn_ = s_bfy[ty + 2][tx], bs_ = s_bfy[ty + 1][tx];
-    T src_x = -C.g * (wc - T(0.5) * (be_ + bw_)) * (be_ - bw_) * C.inv_dx;
-    T src_y = -C.g * (wc - T(0.5) * (bn_ + bs_)) * (bn_ - bs_) * C.inv_dy;
+    // fv_rates (_kernels.py:230-251)
+    T rw = -(S.u.x.fx[0][ty][tx + 1] - S.u.x.fx[0][ty][tx]) * C.inv_dx -
+           (S.u.x.fy[0][ty + 1][tx] - S.u.x.fy[0][ty][tx]) * C.inv_dy;
+    const T src_x = -C.g * (wc - T(0.5) * (be_ + bw_)) * (be_ - bw_) * C.inv_dx;
+    const T src_y = -C.g * (wc - T(0.5) * (bn_ + bs_)) * (bn_ - bs_) * C.inv_dy;
     T h = wc - A.be[o];
     if (h < T(0)) h = T(0);
-    T hstar = h > C.h_eps ? h : C.h_eps;
+    const T hstar = h > C.h_eps ? h : C.h_eps;
     T fric = T(0);
     if (C.c_f > T(0)) fric = C.c_f * sqrt(pc * pc + qc * qc) / (hstar * hstar);
-    T rp = -(s_fx[1][ty][tx + 1] - s_fx[1][ty][tx]) * C.inv_dx -
-           (s_fy[1][ty + 1][tx] - s_fy[1][ty][tx]) * C.inv_dy + src_x - fric * pc;
-    T rq = -(s_fx[2][ty][tx + 1] - s_fx[2][ty][tx]) * C.inv_dx -
-           (s_fy[2][ty + 1][tx] - s_fy[2][ty][tx]) * C.inv_dy + src_y - fric * qc;
+    T rp = -(S.u.x.fx[1][ty][tx + 1] - S.u.x.fx[1][ty][tx]) * C.inv_dx -
+           (S.u.x.fy[1][ty + 1][tx] - S.u.x.fy[1][ty][tx]) * C.inv_dy + src_x - fric * pc;
+    T rq = -(S.u.x.fx[2][ty][tx + 1] - S.u.x.fx[2][ty][tx]) * C.inv_dx -
+           (S.u.x.fy[2][ty + 1][tx] - S.u.x.fy[2][ty][tx]) * C.inv_dy + src_y - fric * qc;
 
     const T d = A.dep[o], dx_ = A.ddx[o], dy_ = A.ddy[o];
     T fs_, gs_;
-    // dispersive_rates (_kernels.py:262-288)
     if (d > T(0)) {
-        const T ec = s_eta[y][x];
-        T e_xx = (s_eta[y][x + 1] - T(2) * ec + s_eta[y][x - 1]) * C.inv_dx2;
-        T e_yy = (s_eta[y + 1][x] - T(2) * ec + s_eta[y - 1][x]) * C.inv_dy2;
-        T e_xy = (s_eta[y + 1][x + 1] - s_eta[y + 1][x - 1] - s_eta[y - 1][x + 1] +
-                  s_eta[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
-        T e_xxx = (s_eta[y][x + 2] - T(2) * s_eta[y][x + 1] + T(2) * s_eta[y][x - 1] -
-                   s_eta[y][x - 2]) * T(0.5) * C.inv_dx * C.inv_dx2;
-        T e_yyy = (s_eta[y + 2][x] - T(2) * s_eta[y + 1][x] + T(2) * s_eta[y - 1][x] -
-                   s_eta[y - 2][x]) * T(0.5) * C.inv_dy * C.inv_dy2;
-        T e_xyy = ((s_eta[y + 1][x + 1] - T(2) * s_eta[y][x + 1] + s_eta[y - 1][x + 1]) -
-                   (s_eta[y + 1][x - 1] - T(2) * s_eta[y][x - 1] + s_eta[y - 1][x - 1])) *
-                  T(0.5) * C.inv_dx * C.inv_dy2;
-        T e_xxy = ((s_eta[y + 1][x + 1] - T(2) * s_eta[y + 1][x] + s_eta[y + 1][x - 1]) -
-                   (s_eta[y - 1][x + 1] - T(2) * s_eta[y - 1][x] + s_eta[y - 1][x - 1])) *
-                  T(0.5) * C.inv_dy * C.inv_dx2;
-        T gd2 = C.g * d * d;
-        T gd3 = gd2 * d;
+        // dispersive_rates (_kernels.py:269-288)
+        const T ec = S.eta[y][x];
+        const T e_xx = (S.eta[y][x + 1] - T(2) * ec + S.eta[y][x - 1]) * C.inv_dx2;
+        const T e_yy = (S.eta[y + 1][x] - T(2) * ec + S.eta[y - 1][x]) * C.inv_dy2;
+        const T e_xy = (S.eta[y + 1][x + 1] - S.eta[y + 1][x - 1] - S.eta[y - 1][x + 1] +
+                        S.eta[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+        const T e_xxx = (S.eta[y][x + 2] - T(2) * S.eta[y][x + 1] + T(2) * S.eta[y][x - 1] -
+                         S.eta[y][x - 2]) * T(0.5) * C.inv_dx * C.inv_dx2;
+        const T e_yyy = (S.eta[y + 2][x] - T(2) * S.eta[y + 1][x] + T(2) * S.eta[y - 1][x] -
+                         S.eta[y - 2][x]) * T(0.5) * C.inv_dy * C.inv_dy2;
+        const T e_xyy = ((S.eta[y + 1][x + 1] - T(2) * S.eta[y][x + 1] + S.eta[y - 1][x + 1]) -
+                         (S.eta[y + 1][x - 1] - T(2) * S.eta[y][x - 1] + S.eta[y - 1][x - 1])) *
+                        T(0.5) * C.inv_dx * C.inv_dy2;
+        const T e_xxy = ((S.eta[y + 1][x + 1] - T(2) * S.eta[y + 1][x] + S.eta[y + 1][x - 1]) -
+                         (S.eta[y - 1][x + 1] - T(2) * S.eta[y - 1][x] + S.eta[y - 1][x - 1])) *
+                        T(0.5) * C.inv_dy * C.inv_dx2;
+        const T gd2 = C.g * d * d;
+        const T gd3 = gd2 * d;
         rp += C.b_disp * gd3 * (e_xxx + e_xyy) +
               C.b_disp * gd2 * (dx_ * (T(2) * e_xx + e_yy) + dy_ * e_xy);
         rq += C.b_disp * gd3 * (e_yyy + e_xxy) +
               C.b_disp * gd2 * (dy_ * (T(2) * e_yy + e_xx) + dx_ * e_xy);
         // cross_rates (_kernels.py:310-321)
-        T q_x = (s_q[y][x + 1] - s_q[y][x - 1]) * T(0.5) * C.inv_dx;
-        T q_y = (s_q[y + 1][x] - s_q[y - 1][x]) * T(0.5) * C.inv_dy;
-        T q_xy = (s_q[y + 1][x + 1] - s_q[y + 1][x - 1] - s_q[y - 1][x + 1] + s_q[y - 1][x - 1]) *
-                 T(0.25) * C.inv_dx * C.inv_dy;
-        T p_x = (s_p[y][x + 1] - s_p[y][x - 1]) * T(0.5) * C.inv_dx;
-        T p_y = (s_p[y + 1][x] - s_p[y - 1][x]) * T(0.5) * C.inv_dy;
-        T p_xy = (s_p[y + 1][x + 1] - s_p[y + 1][x - 1] - s_p[y - 1][x + 1] + s_p[y - 1][x - 1]) *
-                 T(0.25) * C.inv_dx * C.inv_dy;
-        T sixth = div_static(d, C.six, C.r_six);
-        T d2 = C.bp13 * d * d;
+        const T q_x = (S.q[y][x + 1] - S.q[y][x - 1]) * T(0.5) * C.inv_dx;
+        const T q_y = (S.q[y + 1][x] - S.q[y - 1][x]) * T(0.5) * C.inv_dy;
+        const T q_xy = (S.q[y + 1][x + 1] - S.q[y + 1][x - 1] - S.q[y - 1][x + 1] +
+                        S.q[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+        const T p_x = (S.p[y][x + 1] - S.p[y][x - 1]) * T(0.5) * C.inv_dx;
+        const T p_y = (S.p[y + 1][x] - S.p[y - 1][x]) * T(0.5) * C.inv_dy;
+        const T p_xy = (S.p[y + 1][x + 1] - S.p[y + 1][x - 1] - S.p[y - 1][x + 1] +
+                        S.p[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+        const T sixth = div_static(d, C.six, C.r_six);
+        const T d2 = C.bp13 * d * d;
         fs_ = sixth * (dx_ * q_y + dy_ * q_x) + d2 * q_xy;
         gs_ = sixth * (dx_ * p_y + dy_ * p_x) + d2 * p_xy;
     } else {
@@ -256,12 +302,12 @@ __global__ void __launch_bounds__(TX *TY) k_stage(Consts<T> C, const DevParams *
     if (!predict) return;
 
     // U*, V* (dispersion.py:131-148): divisions by grid constants
-    T p_x = div_static(s_p[y][x + 1] - s_p[y][x - 1], C.two_dx, C.r_two_dx);
-    T p_xx = div_static(s_p[y][x + 1] - T(2) * pc + s_p[y][x - 1], C.dx2, C.r_dx2);
-    T ustar = pc - div_static(d * dx_, C.three, C.r_three) * p_x - C.bp13 * d * d * p_xx;
-    T q_y = div_static(s_q[y + 1][x] - s_q[y - 1][x], C.two_dy, C.r_two_dy);
-    T q_yy = div_static(s_q[y + 1][x] - T(2) * qc + s_q[y - 1][x], C.dy2, C.r_dy2);
-    T vstar = qc - div_static(d * dy_, C.three, C.r_three) * q_y - C.bp13 * d * d * q_yy;
+    const T p_x = div_static(S.p[y][x + 1] - S.p[y][x - 1], C.two_dx, C.r_two_dx);
+    const T p_xx = div_static(S.p[y][x + 1] - T(2) * pc + S.p[y][x - 1], C.dx2, C.r_dx2);
+    const T ustar = pc - div_static(d * dx_, C.three, C.r_three) * p_x - C.bp13 * d * d * p_xx;
+    const T q_y = div_static(S.q[y + 1][x] - S.q[y - 1][x], C.two_dy, C.r_two_dy);
+    const T q_yy = div_static(S.q[y + 1][x] - T(2) * qc + S.q[y - 1][x], C.dy2, C.r_dy2);
+    const T vstar = qc - div_static(d * dy_, C.three, C.r_three) * q_y - C.bp13 * d * d * q_yy;
 
     // predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
     T wn, bu, bv, us, vs;
@@ -288,26 +334,19 @@ __global__ void __launch_bounds__(TX *TY) k_stage(Consts<T> C, const DevParams *
     A.vs[o] = vs;
 }
 
-// ---------------------------------------------------------------------------
-// launchers
-
-template <class T>
-void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
-                  const T *sq, T *dw, T *dp, T *dq, cudaStream_t st) {
-    int n = 4 * (C.L.ny + 4) + 4 * C.L.nx;
-    k_ghost<T><<<(n + 127) / 128, 128, 0, st>>>(C, P, which, sw, sp, sq, dw, dp, dq);
-}
-
 template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
                   cudaStream_t st) {
+    const size_t smem = sizeof(StageSmem<T>);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_stage<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
     dim3 grid((C.L.nx + TX - 1) / TX, (C.L.ny + TY - 1) / TY);
-    k_stage<T><<<grid, dim3(TX, TY), 0, st>>>(C, P, A, predict);
+    k_stage<T><<<grid, dim3(TX, TY), smem, st>>>(C, P, A, predict);
 }
 
-template void launch_ghost<double>(const Consts<double> &, const DevParams *, int, const double *,
-                                   const double *, const double *, double *, double *, double *,
-                                   cudaStream_t);
 template void launch_stage<double>(const Consts<double> &, const DevParams *,
                                    const StagePtrs<double> &, int, cudaStream_t);
 
