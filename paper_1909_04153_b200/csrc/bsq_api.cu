@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/bsq.h"
 #include "bsq_launch.h"
 
@@ -74,12 +76,18 @@ struct bsq_ctx {
     int nev;
     float last_ms[kMaxEv];
     int last_n;
+    SolveMaps maps;                    // TMA descriptors (out slots patched per launch)
+    CUtensorMap x_out[3], y_out[3];    // pending P/Q of state 0, state 1; P2/Q2
 
     double *W(int s) { return arr[s ? A_W1 : A_W0]; }
     double *Pp(int s) { return arr[s ? A_P1 : A_P0]; }
     double *Qq(int s) { return arr[s ? A_Q1 : A_Q0]; }
     double *H(int slot, int f) { return arr[A_HIST0 + slot * 5 + f]; }
 };
+
+extern "C" {
+static int build_maps(bsq_ctx *c);
+}
 
 static Layout make_layout(const bsq_desc *d) {
     Layout L;
@@ -354,7 +362,7 @@ int bsq_create(const bsq_desc *desc, const bsq_static *f, void *workspace, size_
         (rc = upload_padded(c, c->arr[A_DDY], f->depth_dy, ny + 4, nx + 4)) ||
         (rc = upload_padded(c, c->arr[A_BFX], f->bed_face_x, ny + 4, nx + 3)) ||
         (rc = upload_padded(c, c->arr[A_BFY], f->bed_face_y, ny + 3, nx + 4)) ||
-        (rc = factor_lines(c, f))) {
+        (rc = factor_lines(c, f)) || (rc = build_maps(c))) {
         std::string keep = g_err;
         bsq_destroy(c);
         return fail(rc, keep);
@@ -488,31 +496,70 @@ static StagePtrs<double> stage_ptrs(bsq_ctx *c, int slot) {
 
 // phase 1 solves U*, V* into the pending state's P, Q; phase 2 solves the
 // corrected right-hand sides (written over us / vs) into P2, Q2.
-static SolvePtrs<double> solve_ptrs(bsq_ctx *c, int phase, int nxt_state) {
+static SolvePtrs<double> solve_ptrs(bsq_ctx *c, int nxt_state) {
     SolvePtrs<double> S;
-    memset(&S, 0, sizeof(S));
-    S.rx = c->arr[A_US];
-    S.ry = c->arr[A_VS];
     S.gp = c->Pp(nxt_state);
     S.gq = c->Qq(nxt_state);
-    S.ax = c->arr[A_AX];
-    S.denx = c->arr[A_DENX];
-    S.rdenx = c->arr[A_RDENX];
-    S.cwx = c->arr[A_CWX];
     S.cx_last = c->cx_last;
-    S.ay = c->arr[A_AY];
-    S.deny = c->arr[A_DENY];
-    S.rdeny = c->arr[A_RDENY];
-    S.cwy = c->arr[A_CWY];
     S.cy_last = c->cy_last;
-    if (phase == 1) {
-        S.outx = c->Pp(nxt_state);
-        S.outy = c->Qq(nxt_state);
-    } else {
-        S.outx = c->arr[A_P2];
-        S.outy = c->arr[A_Q2];
-    }
     return S;
+}
+
+static const SolveMaps &solve_maps(bsq_ctx *c, int phase, int nxt_state) {
+    SolveMaps &M = c->maps;
+    const int k = phase == 1 ? nxt_state : 2;  // out: pending P/Q, or P2/Q2
+    M.x_out = c->x_out[k];
+    M.y_out = c->y_out[k];
+    return M;
+}
+
+// TMA descriptor of the interior region of one pitched array
+static int make_map(CUtensorMap *m, double *base, const Layout &L, bool xdir) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return fail(BSQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint32_t ek = (cuuint32_t)solve_chunk_elems(sizeof(double));
+    cuuint64_t dims[2] = {(cuuint64_t)L.nx, (cuuint64_t)L.ny};
+    cuuint64_t strides[1] = {(cuuint64_t)L.pitch * sizeof(double)};
+    cuuint32_t box[2] = {xdir ? ek : 32u, xdir ? 32u : ek};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base + L.at(GL, GL), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        xdir ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(BSQ_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    return BSQ_OK;
+}
+
+static int build_maps(bsq_ctx *c) {
+    const Layout &L = c->L;
+    SolveMaps &M = c->maps;
+    int rc;
+    if ((rc = make_map(&M.x_rhs, c->arr[A_US], L, true)) ||
+        (rc = make_map(&M.x_a, c->arr[A_AX], L, true)) ||
+        (rc = make_map(&M.x_den, c->arr[A_DENX], L, true)) ||
+        (rc = make_map(&M.x_rden, c->arr[A_RDENX], L, true)) ||
+        (rc = make_map(&M.x_cw, c->arr[A_CWX], L, true)) ||
+        (rc = make_map(&M.y_rhs, c->arr[A_VS], L, false)) ||
+        (rc = make_map(&M.y_a, c->arr[A_AY], L, false)) ||
+        (rc = make_map(&M.y_den, c->arr[A_DENY], L, false)) ||
+        (rc = make_map(&M.y_rden, c->arr[A_RDENY], L, false)) ||
+        (rc = make_map(&M.y_cw, c->arr[A_CWY], L, false)) ||
+        (rc = make_map(&c->x_out[0], c->Pp(0), L, true)) ||
+        (rc = make_map(&c->x_out[1], c->Pp(1), L, true)) ||
+        (rc = make_map(&c->x_out[2], c->arr[A_P2], L, true)) ||
+        (rc = make_map(&c->y_out[0], c->Qq(0), L, false)) ||
+        (rc = make_map(&c->y_out[1], c->Qq(1), L, false)) ||
+        (rc = make_map(&c->y_out[2], c->arr[A_Q2], L, false)))
+        return rc;
+    return BSQ_OK;
 }
 
 static CorrectPtrs<double> correct_ptrs(bsq_ctx *c, int slot, int nxt_state) {
@@ -561,12 +608,12 @@ int bsq_step(bsq_ctx *c, const bsq_step_params *p, bsq_step_result *r) {
     launch_ghost(c->C, c->dparams, 1, c->W(nxt), c->Pp(cur), c->Qq(cur), c->W(nxt), c->Pp(nxt),
                  c->Qq(nxt), c->st);
     ev_mark(c, "ghost_n");
-    launch_solve(c->C, solve_ptrs(c, 1, nxt), c->st);
+    launch_solve(c->C, solve_maps(c, 1, nxt), solve_ptrs(c, nxt), c->st);
     ev_mark(c, "solve1");
     if (c->d.cross_correction) {
         launch_correct(c->C, correct_ptrs(c, slot, nxt), c->st);
         ev_mark(c, "correct");
-        launch_solve(c->C, solve_ptrs(c, 2, nxt), c->st);
+        launch_solve(c->C, solve_maps(c, 2, nxt), solve_ptrs(c, nxt), c->st);
         ev_mark(c, "solve2");
     }
     FinalPtrs<double> F;
@@ -642,8 +689,7 @@ int bsq_solve_momentum(bsq_ctx *c, const double *us, const double *vs, const dou
                        cudaMemcpyHostToDevice, c->st));
     CU(cudaMemcpyAsync(c->Qq(nxt) + L.at(ny + GL, GL), qgn, sizeof(double) * nx,
                        cudaMemcpyHostToDevice, c->st));
-    SolvePtrs<double> S = solve_ptrs(c, 2, nxt);  // into P2 / Q2
-    launch_solve(c->C, S, c->st);
+    launch_solve(c->C, solve_maps(c, 2, nxt), solve_ptrs(c, nxt), c->st);  // into P2 / Q2
     CU(cudaGetLastError());
     if ((rc = download_interior(c, pout, c->arr[A_P2])) ||
         (rc = download_interior(c, qout, c->arr[A_Q2])))

@@ -1,0 +1,84 @@
+// bsq_correct.cu -- cross-correction right-hand sides of the second solve.
+#include <cstdint>
+
+#include "bsq_device.cuh"
+#include "bsq_launch.h"
+
+namespace bsq {
+
+// ---------------------------------------------------------------------------
+// Cross-correction right-hand sides (stepper.py:268-273):
+//   us_corr = base_u + (F*(P1, Q1) - F*_n),  vs_corr = base_v + (G*(P1, Q1) - G*_n)
+// written over us / vs.
+// Each thread owns CR consecutive cells of one column; the 3-column window
+// of P1 and Q1 over rows J-1 .. J+CR is loaded once and shared, and every
+// load is issued before any arithmetic: the kernel is a pure stream.
+constexpr int CR = 2;
+
+template <class T>
+__global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) {
+    const Layout L = C.L;
+    const int I = GL + blockIdx.x * 32 + threadIdx.x;
+    const int J0 = GL + (blockIdx.y * 8 + threadIdx.y) * CR;
+    const long pitch = L.pitch;
+    if (I >= L.nx + GL || J0 >= L.ny + GL) return;
+    T d[CR], dx_[CR], dy_[CR], bu[CR], bv[CR], fs[CR], gs[CR], qw[CR + 2][3], pw[CR + 2][3];
+    const long o0 = L.at(J0, I);
+#pragma unroll
+    for (int r = 0; r < CR + 2; r++)  // rows J0-1 .. J0+CR (rows up to ny+2 exist)
+#pragma unroll
+        for (int b = 0; b < 3; b++) {
+            const long o = o0 + (r - 1) * pitch + (b - 1);
+            const bool in = J0 + r - 1 <= L.ny + GL;
+            qw[r][b] = in ? K.q1[o] : T(0);
+            pw[r][b] = in ? K.p1[o] : T(0);
+        }
+#pragma unroll
+    for (int k = 0; k < CR; k++) {
+        const long o = o0 + k * pitch;
+        const bool in = J0 + k < L.ny + GL;
+        d[k] = in ? K.dep[o] : T(0);
+        dx_[k] = in ? K.ddx[o] : T(0);
+        dy_[k] = in ? K.ddy[o] : T(0);
+        bu[k] = in ? K.bu[o] : T(0);
+        bv[k] = in ? K.bv[o] : T(0);
+        fs[k] = in ? K.fs[o] : T(0);
+        gs[k] = in ? K.gs[o] : T(0);
+    }
+#pragma unroll
+    for (int k = 0; k < CR; k++) {
+        if (J0 + k >= L.ny + GL) continue;
+        T f = T(0), g = T(0);
+        if (d[k] > T(0)) {  // cross_rates (_kernels.py:310-321) on the solved P1, Q1
+            // window row k = J-1, k+1 = J, k+2 = J+1; column 0 = I-1, 1 = I, 2 = I+1
+            const T *qs = qw[k], *qc = qw[k + 1], *qn = qw[k + 2];
+            const T *ps = pw[k], *pc = pw[k + 1], *pn = pw[k + 2];
+            T q_x = (qc[2] - qc[0]) * T(0.5) * C.inv_dx;
+            T q_y = (qn[1] - qs[1]) * T(0.5) * C.inv_dy;
+            T q_xy = (qn[2] - qn[0] - qs[2] + qs[0]) * T(0.25) * C.inv_dx * C.inv_dy;
+            T p_x = (pc[2] - pc[0]) * T(0.5) * C.inv_dx;
+            T p_y = (pn[1] - ps[1]) * T(0.5) * C.inv_dy;
+            T p_xy = (pn[2] - pn[0] - ps[2] + ps[0]) * T(0.25) * C.inv_dx * C.inv_dy;
+            T sixth = div_static(d[k], C.six, C.r_six);
+            T d2 = C.bp13 * d[k] * d[k];
+            f = sixth * (dx_[k] * q_y + dy_[k] * q_x) + d2 * q_xy;
+            g = sixth * (dx_[k] * p_y + dy_[k] * p_x) + d2 * p_xy;
+        }
+        K.us[o0 + k * pitch] = bu[k] + (f - fs[k]);
+        K.vs[o0 + k * pitch] = bv[k] + (g - gs[k]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+template <class T>
+void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st) {
+    dim3 grid((C.L.nx + 31) / 32, (C.L.ny + 8 * CR - 1) / (8 * CR));  // 32 x (8*CR) cells
+    k_correct<T><<<grid, dim3(32, 8), 0, st>>>(C, K);
+}
+
+template void launch_correct<double>(const Consts<double> &, const CorrectPtrs<double> &,
+                                     cudaStream_t);
+
+}  // namespace bsq

@@ -67,8 +67,9 @@ __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, 
     if (h < T(0)) h = T(0);
     const T hstar = h > C.h_eps ? h : C.h_eps;
     const T c = sqrt(C.g * h);
-    const T su = fabs(p) / hstar + c;
-    const T sv = fabs(q) / hstar + c;
+    const T rh = rcp_rn(hstar);  // both quotients correctly rounded via one reciprocal
+    const T su = div_rcp(fabs(p), hstar, rh) + c;
+    const T sv = div_rcp(fabs(q), hstar, rh) + c;
     const double rate = double(nb_max(su * C.inv_dx, sv * C.inv_dy));
     const double speed = double(nb_max(su, sv));
     if (rate > r.rate) r.rate = rate;
@@ -83,14 +84,26 @@ __global__ void __launch_bounds__(FT) k_final(Consts<T> C, FinalPtrs<T> F) {
     const int nx = L.nx, ny = L.ny;
     const int I = GL + blockIdx.x * FX + threadIdx.x;
     Red r{0, 0, 0, 0, 0, 0};
+    // all loads of the thread's cells first (pure stream), then the work
+    T vbe[FR], vw[FR], vp[FR], vq[FR];
+#pragma unroll
+    for (int k = 0; k < FR; k++) {
+        const int J = GL + (blockIdx.y * FR + k) * FY + threadIdx.y;
+        const bool in = I < nx + GL && J < ny + GL;
+        const long o = in ? L.at(J, I) : L.at(GL, GL);
+        vbe[k] = F.be[o];
+        vw[k] = F.w[o];
+        vp[k] = F.pin[o];
+        vq[k] = F.qin[o];
+    }
 #pragma unroll
     for (int k = 0; k < FR; k++) {
         const int J = GL + (blockIdx.y * FR + k) * FY + threadIdx.y;
         if (I >= nx + GL || J >= ny + GL) continue;
         const long o = L.at(J, I);
-        const T be = F.be[o];
-        T w = F.w[o];
-        T p = F.pin[o], q = F.qin[o];
+        const T be = vbe[k];
+        T w = vw[k];
+        T p = vp[k], q = vq[k];
         // clamp and volume tally (stepper.py:281-285); np.maximum keeps NaN
         const T def = be - w;
         if (def > T(0) || def != def) r.clamp = r.clamp + double(def);

@@ -1,5 +1,6 @@
 // bsq_launch.h -- kernel argument bundles and launchers (host-visible).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "bsq_device.cuh"
@@ -20,11 +21,17 @@ struct StagePtrs {
 
 template <class T>
 struct SolvePtrs {
-    const T *rx, *ry;               // folded-later right-hand sides (U*, V* or corrected)
     const T *gp, *gq;               // arrays holding the P / Q ghost values to fold
-    const T *ax, *denx, *rdenx, *cwx, *cx_last;  // x-line LU factors
-    const T *ay, *deny, *rdeny, *cwy, *cy_last;  // y-line LU factors
-    T *outx, *outy;                 // solved P (rows) and Q (columns); also dw scratch
+    const T *cx_last, *cy_last;     // c_{n-1} of every x / y line (ghost folding)
+};
+
+// TMA descriptors of the solve's operands, interior region of each pitched
+// array.  x maps: box {EK, 32} (elements along x, 32 rows), 128-B swizzle;
+// y maps: box {32, EK} (32 columns, elements along y).  `out` is the solved
+// field (also the forward sweep's dw scratch).
+struct SolveMaps {
+    CUtensorMap x_rhs, x_a, x_den, x_rden, x_cw, x_out;
+    CUtensorMap y_rhs, y_a, y_den, y_rden, y_cw, y_out;
 };
 
 template <class T>
@@ -54,7 +61,8 @@ template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
                   cudaStream_t st);
 template <class T>
-void launch_solve(const Consts<T> &C, const SolvePtrs<T> &S, cudaStream_t st);
+void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, cudaStream_t st);
+int solve_chunk_elems(int elem_bytes);
 template <class T>
 void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st);
 template <class T>

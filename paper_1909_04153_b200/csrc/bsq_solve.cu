@@ -1,271 +1,229 @@
-// bsq_solve.cu -- implicit momentum recovery: batched tridiagonal line
-// solves for P (x rows) and Q (y columns), and the cross-correction RHS.
+// bsq_solve.cu -- implicit momentum recovery: batched tridiagonal line solves
+// for P (x rows) and Q (y columns), TMA-pipelined.
 //
-// Reference: implicit.solve_momentum (implicit.py:173-205) with
-// thomas_batch (_kernels.py:360-381); the correction sweep of
-// stepper.py:262-280.
+// Reference: implicit.solve_momentum (implicit.py:173-205) with thomas_batch
+// (_kernels.py:360-381).  The LU factors of the static operator are
+// precomputed on the host with thomas_batch's own arithmetic
+// (den_i = b_i - a_i cw_{i-1}, cw_i = c_i / den_i), so the per-step forward
+// sweep dw_i = (r_i - a_i dw_{i-1}) / den_i and back substitution
+// x_i = dw_i - cw_i x_{i+1} reproduce thomas_batch bit for bit; the division
+// by the static pivot is div_static (correctly rounded, Markstein).
+//
+// A CTA owns 32 lines (x: 32 consecutive rows; y: 32 consecutive columns)
+// and has two warps:
+//   producer (warp 1, one elected lane) streams 2-D tiles of 32 lines x EK
+//     elements with bulk tensor copies (TMA) into an NS-deep smem ring,
+//     gated by full/empty mbarriers -- up to NS-1 tiles per array in flight
+//     without holding a single register;
+//   consumer (warp 0): lane l runs line l's recurrence out of the ring, folds
+//     the boundary ghosts into the first/last element, writes results into a
+//     double-buffered out tile and TMA-stores it.
+// x tiles use the 128-byte swizzle so the consumer's column walk through a
+// row-major tile is (nearly) bank-conflict free; y tiles are naturally
+// [element][line].  Out-of-range lines/elements are zero-filled on load and
+// clipped on store by the TMA unit.  The forward sweep's dw is stored into
+// the output array and read back by the backward sweep, which overwrites it.
 #include <cstdint>
 
 #include "bsq_device.cuh"
 #include "bsq_launch.h"
+#include "bsq_tma.cuh"
 
 namespace bsq {
 
-// ---------------------------------------------------------------------------
-// Warp-specialized pipelined line solve.
-//
-// A CTA owns 32 lines (x: 32 consecutive rows; y: 32 consecutive columns).
-// Warp 0 is the consumer: lane l runs line l's Thomas recurrence entirely out
-// of shared memory.  Warps 1..8 are producers: per chunk of SK elements each
-// producer thread owns exactly four (line, element) items and issues all of
-// their global loads before touching shared memory, so a chunk's 32 KB are in
-// flight at once; the folded right-hand side is assembled on the way in.
-// Chunks are double buffered: while the consumer sweeps chunk c, producers
-// fill chunk c+1 and drain chunk c-1.
-//
-// The LU factors of the static operator are precomputed on the host with
-// thomas_batch's own arithmetic (den_i = b_i - a_i cw_{i-1},
-// cw_i = c_i / den_i), so the per-step forward sweep
-// dw_i = (r_i - a_i dw_{i-1}) / den_i and back substitution
-// x_i = dw_i - cw_i x_{i+1} reproduce thomas_batch bit for bit.  The division
-// by the static pivot uses div_static (correctly rounded).  The forward
-// sweep's dw is parked in the output array and overwritten by x.
-constexpr int SK = 32;                 // chunk length (elements per line)
-constexpr int SLD = SK + 1;            // padded smem row: conflict-free access
-constexpr int SW = 9;                  // warps per CTA: 1 consumer + 8 producers
-constexpr int NPROD = (SW - 1) * 32;   // producer threads
-constexpr int ITEMS = 32 * SK / NPROD; // items per producer thread per chunk
-constexpr int SBUF = 32 * SLD;
-static_assert(ITEMS * NPROD == 32 * SK, "producer items must tile the chunk");
+constexpr int NLINE = 32;  // lines per CTA
+constexpr int NS = 6;      // forward ring depth (stages of 4 tiles)
+constexpr int NS2 = 12;    // backward ring depth (stages of 2 tiles), same bytes
 
 template <class T>
-struct SolveSmem {
-    T r[2][SBUF], a[2][SBUF], den[2][SBUF], rden[2][SBUF], out[2][SBUF];
+struct TileGeom {
+    static constexpr int EK = 128 / sizeof(T);              // elements per chunk (one 128-B row)
+    static constexpr int TILE = NLINE * EK;                  // elements per tile
+    static constexpr int TILE_B = TILE * sizeof(T);          // 4096 bytes
+    static constexpr int RING_B = NS * 4 * TILE_B;           // == NS2 * 2 * TILE_B
+    static constexpr int SMEM_B = 1024 + RING_B + 2 * TILE_B + 8 * (2 * NS + 2 * NS2);
 };
 
-template <bool XDIR>
-__device__ __forceinline__ int tile_idx(int line, int k) {
-    // x: [line][k]: a producer warp writes one row segment, the consumer
-    //    reads a padded column (stride SLD: conflict-free)
-    // y: [k][line]: both sides touch 32 consecutive doubles
-    return XDIR ? line * SLD + k : k * SLD + line;
-}
-
-template <bool XDIR>
-__device__ __forceinline__ void item_of(int it, int &ln, int &k) {
-    // consecutive producer lanes -> consecutive global addresses
-    if (XDIR) { ln = it >> 5; k = it & 31; } else { k = it >> 5; ln = it & 31; }
+// element offset of (line ln, chunk element k) inside a tile
+template <class T, bool XDIR>
+__device__ __forceinline__ int toff(int ln, int k) {
+    if (XDIR) {  // box {EK, 32}: row = line, 128-B swizzle of 16-B units by (row & 7)
+        constexpr int PER16 = 16 / sizeof(T);
+        const int unit = (k / PER16) ^ (ln & 7);
+        return ln * TileGeom<T>::EK + unit * PER16 + (k % PER16);
+    }
+    return k * NLINE + ln;  // box {32, EK}: row = element
 }
 
 template <class T, bool XDIR>
-__device__ void solve_lines(const Consts<T> &C, const SolvePtrs<T> &S, int line0, SolveSmem<T> &sm) {
+__device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
+                                int line0, unsigned char *smem) {
+    using G = TileGeom<T>;
+    constexpr int EK = G::EK, TILE = G::TILE;
     const Layout L = C.L;
-    const int n = XDIR ? L.nx : L.ny;  // line length
+    const int n = XDIR ? L.nx : L.ny;
     const int nlines = XDIR ? L.ny : L.nx;
-    const int nc = (n + SK - 1) / SK;
+    const int nc = (n + EK - 1) / EK;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ptid = threadIdx.x - 32;
-    const T *__restrict__ rhs = XDIR ? S.rx : S.ry;
-    const T *__restrict__ A = XDIR ? S.ax : S.ay;
-    const T *__restrict__ DEN = XDIR ? S.denx : S.deny;
-    const T *__restrict__ RDEN = XDIR ? S.rdenx : S.rdeny;
-    const T *__restrict__ CW = XDIR ? S.cwx : S.cwy;
-    const T *__restrict__ clast = XDIR ? S.cx_last : S.cy_last;
-    T *out = XDIR ? S.outx : S.outy;
 
-    auto offset = [&](int line, int e) -> long {
-        return XDIR ? L.at(GL + line, GL + e) : L.at(GL + e, GL + line);
+    T *ring = reinterpret_cast<T *>(smem);                    // NS x {r, a, den, rden}
+    T *outb = reinterpret_cast<T *>(smem + G::RING_B);        // 2 out tiles
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::RING_B + 2 * G::TILE_B);
+    uint64_t *empty = full + NS;
+    uint64_t *full2 = empty + NS;
+    uint64_t *empty2 = full2 + NS2;
+
+    const CUtensorMap *m_rhs = XDIR ? &M.x_rhs : &M.y_rhs;
+    const CUtensorMap *m_a = XDIR ? &M.x_a : &M.y_a;
+    const CUtensorMap *m_den = XDIR ? &M.x_den : &M.y_den;
+    const CUtensorMap *m_rden = XDIR ? &M.x_rden : &M.y_rden;
+    const CUtensorMap *m_cw = XDIR ? &M.x_cw : &M.y_cw;
+    const CUtensorMap *m_out = XDIR ? &M.x_out : &M.y_out;
+    auto coords = [&](int c, int &c0, int &c1) {
+        if (XDIR) { c0 = c * EK; c1 = line0; } else { c0 = line0; c1 = c * EK; }
     };
 
-    // producers: chunk c of r, a, den, rden into buffer b; drain chunk d of
-    // out (d < 0: none).  All loads first, then the drain, then smem stores.
-    auto fill_fwd = [&](int c, int b, int d, int bd) {
-        T rv[ITEMS], av[ITEMS], dv[ITEMS], qv[ITEMS];
-        long ov[ITEMS];
-        bool okv[ITEMS];
-#pragma unroll
-        for (int u = 0; u < ITEMS; u++) {
-            int ln, k;
-            item_of<XDIR>(u * NPROD + ptid, ln, k);
-            const int line = line0 + ln, e = c * SK + k;
-            okv[u] = c < nc && line < nlines && e < n;
-            ov[u] = okv[u] ? offset(line, e) : 0;
-            rv[u] = okv[u] ? rhs[ov[u]] : T(0);
-            av[u] = okv[u] ? A[ov[u]] : T(0);
-            dv[u] = okv[u] ? DEN[ov[u]] : T(1);
-            qv[u] = okv[u] ? RDEN[ov[u]] : T(1);
-        }
-        if (d >= 0) {
-#pragma unroll
-            for (int u = 0; u < ITEMS; u++) {
-                int ln, k;
-                item_of<XDIR>(u * NPROD + ptid, ln, k);
-                const int line = line0 + ln, e = d * SK + k;
-                if (line < nlines && e < n) out[offset(line, e)] = sm.out[bd][tile_idx<XDIR>(ln, k)];
-            }
-        }
-        if (c >= nc) return;
-#pragma unroll
-        for (int u = 0; u < ITEMS; u++) {
-            int ln, k;
-            item_of<XDIR>(u * NPROD + ptid, ln, k);
-            const int line = line0 + ln, e = c * SK + k;
-            T r = rv[u];
-            if (okv[u] && e == 0) {  // implicit.py:178 / :190 ghost folding
-                const T g0 = XDIR ? S.gp[L.at(GL + line, GL - 1)] : S.gq[L.at(GL - 1, GL + line)];
-                r = r - av[u] * g0;
-            }
-            if (okv[u] && e == n - 1) {
-                const T g1 = XDIR ? S.gp[L.at(GL + line, n + GL)] : S.gq[L.at(n + GL, GL + line)];
-                r = r - clast[line] * g1;
-            }
-            const int t = tile_idx<XDIR>(ln, k);
-            sm.r[b][t] = r;
-            sm.a[b][t] = av[u];
-            sm.den[b][t] = dv[u];
-            sm.rden[b][t] = qv[u];
-        }
-    };
-    // producers: chunk c of (dw parked in out, cw) into buffer b; drain chunk d
-    auto fill_bwd = [&](int c, int b, int d, int bd) {
-        T dwv[ITEMS], cwv[ITEMS];
-#pragma unroll
-        for (int u = 0; u < ITEMS; u++) {
-            int ln, k;
-            item_of<XDIR>(u * NPROD + ptid, ln, k);
-            const int line = line0 + ln, e = c * SK + k;
-            const bool ok = c >= 0 && line < nlines && e < n;
-            const long o = ok ? offset(line, e) : 0;
-            dwv[u] = ok ? out[o] : T(0);
-            cwv[u] = ok ? CW[o] : T(0);
-        }
-        if (d >= 0) {
-#pragma unroll
-            for (int u = 0; u < ITEMS; u++) {
-                int ln, k;
-                item_of<XDIR>(u * NPROD + ptid, ln, k);
-                const int line = line0 + ln, e = d * SK + k;
-                if (line < nlines && e < n) out[offset(line, e)] = sm.out[bd][tile_idx<XDIR>(ln, k)];
-            }
-        }
-        if (c < 0) return;
-#pragma unroll
-        for (int u = 0; u < ITEMS; u++) {
-            int ln, k;
-            item_of<XDIR>(u * NPROD + ptid, ln, k);
-            const int t = tile_idx<XDIR>(ln, k);
-            sm.r[b][t] = dwv[u];
-            sm.a[b][t] = cwv[u];
-        }
-    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < NS2; s++) { mbar_init(&full2[s], 1); mbar_init(&empty2[s], 1); }
+        fence_mbar_init();
+    }
+    __syncthreads();
 
     // ---- forward sweep --------------------------------------------------------
-    if (warp > 0) fill_fwd(0, 0, -1, 0);
-    __syncthreads();
-    T dw = T(0);
-    for (int c = 0; c < nc; c++) {
-        const int b = c & 1;
-        if (warp == 0) {
-            const int kmax = min(SK, n - c * SK);
-            if (kmax == SK) {
-#pragma unroll 8
-                for (int k = 0; k < SK; k++) {
-                    const int t = tile_idx<XDIR>(lane, k);
-                    const T r = sm.r[b][t];
-                    const T num = (c == 0 && k == 0) ? r : r - sm.a[b][t] * dw;
-                    dw = div_static(num, sm.den[b][t], sm.rden[b][t]);
-                    sm.out[b][t] = dw;
-                }
-            } else {
-                for (int k = 0; k < kmax; k++) {
-                    const int t = tile_idx<XDIR>(lane, k);
-                    const T r = sm.r[b][t];
-                    const T num = (c == 0 && k == 0) ? r : r - sm.a[b][t] * dw;
-                    dw = div_static(num, sm.den[b][t], sm.rden[b][t]);
-                    sm.out[b][t] = dw;
-                }
+    if (warp == 1) {
+        if (lane == 0) {
+            for (int c = 0; c < nc; c++) {
+                const int s = c % NS;
+                if (c >= NS) mbar_wait(&empty[s], ((c / NS) - 1) & 1);
+                mbar_expect_tx(&full[s], 4 * G::TILE_B);
+                int c0, c1;
+                coords(c, c0, c1);
+                T *st = ring + s * 4 * TILE;
+                tma_load_2d(st, m_rhs, c0, c1, &full[s]);
+                tma_load_2d(st + TILE, m_a, c0, c1, &full[s]);
+                tma_load_2d(st + 2 * TILE, m_den, c0, c1, &full[s]);
+                tma_load_2d(st + 3 * TILE, m_rden, c0, c1, &full[s]);
             }
-        } else {
-            fill_fwd(c + 1, b ^ 1, c - 1, b ^ 1);
         }
-        __syncthreads();
+    } else {
+        const int line = line0 + lane;
+        const bool lv = line < nlines;
+        // ghost values folded into the first/last element (implicit.py:178-179, :190-191)
+        const T g0 = !lv ? T(0) : XDIR ? S.gp[L.at(GL + line, GL - 1)] : S.gq[L.at(GL - 1, GL + line)];
+        const T g1 = !lv ? T(0) : XDIR ? S.gp[L.at(GL + line, n + GL)] : S.gq[L.at(n + GL, GL + line)];
+        const T cl = !lv ? T(0) : XDIR ? S.cx_last[line] : S.cy_last[line];
+        T dw = T(0);
+        for (int c = 0; c < nc; c++) {
+            const int s = c % NS;
+            T *st = ring + s * 4 * TILE;
+            T *ob = outb + (c & 1) * TILE;
+            if (lane == 0) bulk_wait_read<1>();  // the store from this out tile (c-2) has read it
+            __syncwarp();
+            mbar_wait(&full[s], (c / NS) & 1);
+            const int kmax = min(EK, n - c * EK);
+#pragma unroll 4
+            for (int k = 0; k < kmax; k++) {
+                const int t = toff<T, XDIR>(lane, k);
+                T r = st[t];
+                const T a = st[TILE + t];
+                const int e = c * EK + k;
+                if (e == 0) r = r - a * g0;
+                if (e == n - 1) r = r - cl * g1;
+                const T num = e == 0 ? r : r - a * dw;
+                dw = div_static(num, st[2 * TILE + t], st[3 * TILE + t]);
+                ob[t] = dw;
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&empty[s]);
+                int c0, c1;
+                coords(c, c0, c1);
+                tma_store_2d(m_out, c0, c1, ob);
+                bulk_commit();
+            }
+        }
+        if (lane == 0) {
+            bulk_wait_all();  // dw globally written before the backward loads read it
+            fence_async_global();
+        }
     }
-    // drain the last forward chunk while loading the last chunk for the back sweep
-    if (warp > 0) fill_bwd(-1, 0, nc - 1, (nc - 1) & 1);
     __syncthreads();
 
-    // ---- back substitution (chunks in reverse) ---------------------------------
-    if (warp > 0) fill_bwd(nc - 1, 0, -1, 0);
-    __syncthreads();
-    T xv = T(0);
-    for (int s = 0; s < nc; s++) {
-        const int c = nc - 1 - s, b = s & 1;
-        if (warp == 0) {
-            const int kmax = min(SK, n - c * SK);
-            for (int k = kmax - 1; k >= 0; k--) {
-                const int t = tile_idx<XDIR>(lane, k);
-                xv = (s == 0 && k == kmax - 1) ? sm.r[b][t] : sm.r[b][t] - sm.a[b][t] * xv;
-                sm.out[b][t] = xv;
+    // ---- back substitution (chunks in reverse) -----------------------------------
+    if (warp == 1) {
+        if (lane == 0) {
+            for (int s_ = 0; s_ < nc; s_++) {
+                const int c = nc - 1 - s_, s = s_ % NS2;
+                if (s_ >= NS2) mbar_wait(&empty2[s], ((s_ / NS2) - 1) & 1);
+                mbar_expect_tx(&full2[s], 2 * G::TILE_B);
+                int c0, c1;
+                coords(c, c0, c1);
+                T *st = ring + s * 2 * TILE;
+                tma_load_2d(st, m_out, c0, c1, &full2[s]);
+                tma_load_2d(st + TILE, m_cw, c0, c1, &full2[s]);
             }
-        } else {
-            fill_bwd(c - 1, b ^ 1, s >= 1 ? c + 1 : -1, b ^ 1);
         }
-        __syncthreads();
+    } else {
+        T xv = T(0);
+        for (int s_ = 0; s_ < nc; s_++) {
+            const int c = nc - 1 - s_, s = s_ % NS2;
+            T *st = ring + s * 2 * TILE;
+            T *ob = outb + (s_ & 1) * TILE;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            mbar_wait(&full2[s], (s_ / NS2) & 1);
+            const int kmax = min(EK, n - c * EK);
+#pragma unroll 4
+            for (int k = kmax - 1; k >= 0; k--) {
+                const int t = toff<T, XDIR>(lane, k);
+                const T dwk = st[t];
+                xv = (s_ == 0 && k == kmax - 1) ? dwk : dwk - st[TILE + t] * xv;
+                ob[t] = xv;
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&empty2[s]);
+                int c0, c1;
+                coords(c, c0, c1);
+                tma_store_2d(m_out, c0, c1, ob);
+                bulk_commit();
+            }
+        }
+        if (lane == 0) bulk_wait_all();
     }
-    if (warp > 0) fill_bwd(-1, 0, 0, (nc - 1) & 1);
 }
 
 // Blocks [0, nbx) take x lines (rows -> P); blocks [nbx, ...) y lines (columns -> Q).
 template <class T>
-__global__ void __launch_bounds__(SW * 32, 2) k_solve_pipe(Consts<T> C, SolvePtrs<T> S, int nbx) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SolveSmem<T> &sm = *reinterpret_cast<SolveSmem<T> *>(smem_raw);
+__global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_constant__ SolveMaps M,
+                                                  SolvePtrs<T> S, int nbx) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     if ((int)blockIdx.x < nbx)
-        solve_lines<T, true>(C, S, blockIdx.x * 32, sm);
+        solve_lines_tma<T, true>(C, M, S, blockIdx.x * NLINE, smem);
     else
-        solve_lines<T, false>(C, S, (blockIdx.x - nbx) * 32, sm);
+        solve_lines_tma<T, false>(C, M, S, (blockIdx.x - nbx) * NLINE, smem);
 }
 
-// ---------------------------------------------------------------------------
-// Cross-correction right-hand sides (stepper.py:268-273):
-//   us_corr = base_u + (F*(P1, Q1) - F*_n),  vs_corr = base_v + (G*(P1, Q1) - G*_n)
-// written over us / vs.
 template <class T>
-__global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) {
-    const Layout L = C.L;
-    const int I = GL + blockIdx.x * 32 + threadIdx.x, J = GL + blockIdx.y * 8 + threadIdx.y;
-    if (I >= L.nx + GL || J >= L.ny + GL) return;
-    const long o = L.at(J, I);
-    const T d = K.dep[o], dx_ = K.ddx[o], dy_ = K.ddy[o];
-    const T fs = cross_f(C, K.q1, o, d, dx_, dy_);
-    const T gs = cross_g(C, K.p1, o, d, dx_, dy_);
-    K.us[o] = K.bu[o] + (fs - K.fs[o]);
-    K.vs[o] = K.bv[o] + (gs - K.gs[o]);
-}
-
-// ---------------------------------------------------------------------------
-// launchers
-
-template <class T>
-void launch_solve(const Consts<T> &C, const SolvePtrs<T> &S, cudaStream_t st) {
-    const int nbx = (C.L.ny + 31) / 32, nby = (C.L.nx + 31) / 32;
-    const size_t smem = sizeof(SolveSmem<T>);
+void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, cudaStream_t st) {
+    const int nbx = (C.L.ny + NLINE - 1) / NLINE, nby = (C.L.nx + NLINE - 1) / NLINE;
+    const int smem = TileGeom<T>::SMEM_B;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_solve_pipe<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_solve_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    k_solve_pipe<T><<<nbx + nby, SW * 32, smem, st>>>(C, S, nbx);
+    k_solve_tma<T><<<nbx + nby, 64, smem, st>>>(C, M, S, nbx);
 }
 
-template <class T>
-void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st) {
-    dim3 grid((C.L.nx + 31) / 32, (C.L.ny + 7) / 8);
-    k_correct<T><<<grid, dim3(32, 8), 0, st>>>(C, K);
-}
+int solve_chunk_elems(int elem_bytes) { return 128 / elem_bytes; }
 
-template void launch_solve<double>(const Consts<double> &, const SolvePtrs<double> &, cudaStream_t);
-template void launch_correct<double>(const Consts<double> &, const CorrectPtrs<double> &,
-                                     cudaStream_t);
+template void launch_solve<double>(const Consts<double> &, const SolveMaps &,
+                                   const SolvePtrs<double> &, cudaStream_t);
 
 }  // namespace bsq

@@ -54,20 +54,6 @@ struct StageSmem {
     } u;
 };
 
-// Markstein quotient x/d from r = RN(1/d), robust to non-finite x: a
-// non-finite product returns IEEE's x/d (inf or NaN) so the non-finite
-// stage scan sees exactly the reference's cells.
-template <class T>
-__device__ __forceinline__ T div_rcp(T x, T d, T r) {
-    T q0 = x * r;
-    T e = fma_rn(-q0, d, x);
-    T q1 = fma_rn(e, r, q0);
-    return (e == T(0) || q1 != q1) ? q0 : q1;
-}
-
-__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
-__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
-
 // cu_flux (bsq_device.cuh) with the two divisions by each side's depth
 // sharing one correctly rounded reciprocal: ul = nl/dl and nl*tl/dl are
 // still the correctly rounded quotients.
