@@ -70,6 +70,7 @@ struct bsq_ctx {
     int pend_slot;
     bool pending;
     bool singular;
+    bool pos_pivots;  // every Thomas pivot > 0: select-free division in the solves
     bool timing;
     cudaEvent_t ev[kMaxEv];
     const char *ev_name[kMaxEv];
@@ -216,7 +217,7 @@ static int factor_lines(bsq_ctx *c, const bsq_static *f) {
     std::vector<double> ay(E, 0.0), deny(E, 1.0), rdeny(E, 1.0), cwy(E, 0.0);
     std::vector<double> cxl(ny), cyl(nx);
     const double six_dx = 6.0 * c->d.dx, six_dy = 6.0 * c->d.dy;
-    bool singular = false;
+    bool singular = false, pos = true;
     for (int j = 0; j < ny; j++) {  // x rows
         double cw_prev = 0.0;
         for (int i = 0; i < nx; i++) {
@@ -229,7 +230,8 @@ static int factor_lines(bsq_ctx *c, const bsq_static *f) {
             double cw = cc / den;
             ax[o] = a;
             denx[o] = den;
-            rdenx[o] = 1.0 / den;
+            rdenx[o] = -(1.0 / den);  // stored negated (div_static_pos)
+            if (!(den > 0.0)) pos = false;
             cwx[o] = cw;
             cw_prev = cw;
             if (i == nx - 1) cxl[j] = cc;
@@ -247,13 +249,15 @@ static int factor_lines(bsq_ctx *c, const bsq_static *f) {
             double cw = cc / den;
             ay[o] = a;
             deny[o] = den;
-            rdeny[o] = 1.0 / den;
+            rdeny[o] = -(1.0 / den);
+            if (!(den > 0.0)) pos = false;
             cwy[o] = cw;
             cw_prev = cw;
             if (j == ny - 1) cyl[i] = cc;
         }
     }
     c->singular = singular;
+    c->pos_pivots = pos;
     const size_t B = sizeof(double) * E;
     CU(cudaMemcpyAsync(c->arr[A_AX], ax.data(), B, cudaMemcpyHostToDevice, c->st));
     CU(cudaMemcpyAsync(c->arr[A_DENX], denx.data(), B, cudaMemcpyHostToDevice, c->st));
@@ -608,12 +612,12 @@ int bsq_step(bsq_ctx *c, const bsq_step_params *p, bsq_step_result *r) {
     launch_ghost(c->C, c->dparams, 1, c->W(nxt), c->Pp(cur), c->Qq(cur), c->W(nxt), c->Pp(nxt),
                  c->Qq(nxt), c->st);
     ev_mark(c, "ghost_n");
-    launch_solve(c->C, solve_maps(c, 1, nxt), solve_ptrs(c, nxt), c->st);
+    launch_solve(c->C, solve_maps(c, 1, nxt), solve_ptrs(c, nxt), c->pos_pivots, c->st);
     ev_mark(c, "solve1");
     if (c->d.cross_correction) {
         launch_correct(c->C, correct_ptrs(c, slot, nxt), c->st);
         ev_mark(c, "correct");
-        launch_solve(c->C, solve_maps(c, 2, nxt), solve_ptrs(c, nxt), c->st);
+        launch_solve(c->C, solve_maps(c, 2, nxt), solve_ptrs(c, nxt), c->pos_pivots, c->st);
         ev_mark(c, "solve2");
     }
     FinalPtrs<double> F;
@@ -689,7 +693,7 @@ int bsq_solve_momentum(bsq_ctx *c, const double *us, const double *vs, const dou
                        cudaMemcpyHostToDevice, c->st));
     CU(cudaMemcpyAsync(c->Qq(nxt) + L.at(ny + GL, GL), qgn, sizeof(double) * nx,
                        cudaMemcpyHostToDevice, c->st));
-    launch_solve(c->C, solve_maps(c, 2, nxt), solve_ptrs(c, nxt), c->st);  // into P2 / Q2
+    launch_solve(c->C, solve_maps(c, 2, nxt), solve_ptrs(c, nxt), c->pos_pivots, c->st);  // into P2 / Q2
     CU(cudaGetLastError());
     if ((rc = download_interior(c, pout, c->arr[A_P2])) ||
         (rc = download_interior(c, qout, c->arr[A_Q2])))

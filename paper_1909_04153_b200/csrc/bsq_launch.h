@@ -61,7 +61,8 @@ template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
                   cudaStream_t st);
 template <class T>
-void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, cudaStream_t st);
+void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, bool pos_pivots,
+                  cudaStream_t st);
 int solve_chunk_elems(int elem_bytes);
 template <class T>
 void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st);

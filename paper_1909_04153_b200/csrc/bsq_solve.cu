@@ -55,7 +55,7 @@ __device__ __forceinline__ int toff(int ln, int k) {
     return k * NLINE + ln;  // box {32, EK}: row = element
 }
 
-template <class T, bool XDIR>
+template <class T, bool XDIR, bool POS>
 __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
                                 int line0, unsigned char *smem) {
     using G = TileGeom<T>;
@@ -113,6 +113,10 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
         const T g0 = !lv ? T(0) : XDIR ? S.gp[L.at(GL + line, GL - 1)] : S.gq[L.at(GL - 1, GL + line)];
         const T g1 = !lv ? T(0) : XDIR ? S.gp[L.at(GL + line, n + GL)] : S.gq[L.at(n + GL, GL + line)];
         const T cl = !lv ? T(0) : XDIR ? S.cx_last[line] : S.cy_last[line];
+        // dw_i = (r_i - a_i dw_{i-1}) / den_i; the ring holds nr = -RN(1/den)
+        auto step = [&](T num, T den, T nr) -> T {
+            return POS ? div_static_pos(num, den, nr) : div_static(num, den, -nr);
+        };
         T dw = T(0);
         for (int c = 0; c < nc; c++) {
             const int s = c % NS;
@@ -122,16 +126,32 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
             __syncwarp();
             mbar_wait(&full[s], (c / NS) & 1);
             const int kmax = min(EK, n - c * EK);
-#pragma unroll 4
-            for (int k = 0; k < kmax; k++) {
-                const int t = toff<T, XDIR>(lane, k);
-                T r = st[t];
-                const T a = st[TILE + t];
-                const int e = c * EK + k;
-                if (e == 0) r = r - a * g0;
-                if (e == n - 1) r = r - cl * g1;
-                const T num = e == 0 ? r : r - a * dw;
-                dw = div_static(num, st[2 * TILE + t], st[3 * TILE + t]);
+            int k0 = 0, kend = kmax;
+            if (c == 0) {  // first element: folded, no recurrence term (thomas_batch dw[0])
+                const int t = toff<T, XDIR>(lane, 0);
+                dw = step(st[t] - st[TILE + t] * g0, st[2 * TILE + t], st[3 * TILE + t]);
+                ob[t] = dw;
+                k0 = 1;
+            }
+            if (c == nc - 1) kend = kmax - 1;  // last element peeled below
+            if (k0 == 0 && kend == EK) {
+#pragma unroll
+                for (int k = 0; k < EK; k++) {
+                    const int t = toff<T, XDIR>(lane, k);
+                    dw = step(st[t] - st[TILE + t] * dw, st[2 * TILE + t], st[3 * TILE + t]);
+                    ob[t] = dw;
+                }
+            } else {
+                for (int k = k0; k < kend; k++) {
+                    const int t = toff<T, XDIR>(lane, k);
+                    dw = step(st[t] - st[TILE + t] * dw, st[2 * TILE + t], st[3 * TILE + t]);
+                    ob[t] = dw;
+                }
+            }
+            if (c == nc - 1) {  // last element: fold the far ghost
+                const int t = toff<T, XDIR>(lane, kmax - 1);
+                const T r = st[t] - cl * g1;
+                dw = step(r - st[TILE + t] * dw, st[2 * TILE + t], st[3 * TILE + t]);
                 ob[t] = dw;
             }
             fence_async_smem();
@@ -175,12 +195,26 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
             __syncwarp();
             mbar_wait(&full2[s], (s_ / NS2) & 1);
             const int kmax = min(EK, n - c * EK);
-#pragma unroll 4
-            for (int k = kmax - 1; k >= 0; k--) {
-                const int t = toff<T, XDIR>(lane, k);
-                const T dwk = st[t];
-                xv = (s_ == 0 && k == kmax - 1) ? dwk : dwk - st[TILE + t] * xv;
+            int ktop = kmax - 1;
+            if (s_ == 0) {  // out[n-1] = dw[n-1]
+                const int t = toff<T, XDIR>(lane, ktop);
+                xv = st[t];
                 ob[t] = xv;
+                ktop--;
+            }
+            if (ktop == EK - 1) {
+#pragma unroll
+                for (int k = EK - 1; k >= 0; k--) {
+                    const int t = toff<T, XDIR>(lane, k);
+                    xv = st[t] - st[TILE + t] * xv;
+                    ob[t] = xv;
+                }
+            } else {
+                for (int k = ktop; k >= 0; k--) {
+                    const int t = toff<T, XDIR>(lane, k);
+                    xv = st[t] - st[TILE + t] * xv;
+                    ob[t] = xv;
+                }
             }
             fence_async_smem();
             __syncwarp();
@@ -197,33 +231,40 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
 }
 
 // Blocks [0, nbx) take x lines (rows -> P); blocks [nbx, ...) y lines (columns -> Q).
-template <class T>
+template <class T, bool POS>
 __global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_constant__ SolveMaps M,
                                                   SolvePtrs<T> S, int nbx) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     if ((int)blockIdx.x < nbx)
-        solve_lines_tma<T, true>(C, M, S, blockIdx.x * NLINE, smem);
+        solve_lines_tma<T, true, POS>(C, M, S, blockIdx.x * NLINE, smem);
     else
-        solve_lines_tma<T, false>(C, M, S, (blockIdx.x - nbx) * NLINE, smem);
+        solve_lines_tma<T, false, POS>(C, M, S, (blockIdx.x - nbx) * NLINE, smem);
 }
 
+// pos_pivots: every Thomas pivot of both operators is > 0 (host-checked), which
+// enables the select-free quotient on the recurrence's critical path.
 template <class T>
-void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, cudaStream_t st) {
+void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, bool pos_pivots,
+                  cudaStream_t st) {
     const int nbx = (C.L.ny + NLINE - 1) / NLINE, nby = (C.L.nx + NLINE - 1) / NLINE;
     const int smem = TileGeom<T>::SMEM_B;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_solve_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_solve_tma<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_solve_tma<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
-    k_solve_tma<T><<<nbx + nby, 64, smem, st>>>(C, M, S, nbx);
+    if (pos_pivots)
+        k_solve_tma<T, true><<<nbx + nby, 64, smem, st>>>(C, M, S, nbx);
+    else
+        k_solve_tma<T, false><<<nbx + nby, 64, smem, st>>>(C, M, S, nbx);
 }
 
 int solve_chunk_elems(int elem_bytes) { return 128 / elem_bytes; }
 
 template void launch_solve<double>(const Consts<double> &, const SolveMaps &,
-                                   const SolvePtrs<double> &, cudaStream_t);
+                                   const SolvePtrs<double> &, bool, cudaStream_t);
 
 }  // namespace bsq
