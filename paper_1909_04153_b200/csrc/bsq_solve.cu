@@ -126,34 +126,43 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
             __syncwarp();
             mbar_wait(&full[s], (c / NS) & 1);
             const int kmax = min(EK, n - c * EK);
-            int k0 = 0, kend = kmax;
-            if (c == 0) {  // first element: folded, no recurrence term (thomas_batch dw[0])
-                const int t = toff<T, XDIR>(lane, 0);
-                dw = step(st[t] - st[TILE + t] * g0, st[2 * TILE + t], st[3 * TILE + t]);
-                ob[t] = dw;
-                k0 = 1;
+            // the whole chunk goes to registers first: the ring and the out tile
+            // share one smem base, so interleaved loads could not be hoisted past
+            // the stores and every element would pay an LDS round trip on the chain
+            T rv[EK], av[EK], dv[EK], nv[EK];
+#pragma unroll
+            for (int k = 0; k < EK; k++) {
+                const int t = toff<T, XDIR>(lane, k);
+                rv[k] = st[t];
+                av[k] = st[TILE + t];
+                dv[k] = st[2 * TILE + t];
+                nv[k] = st[3 * TILE + t];
             }
-            if (c == nc - 1) kend = kmax - 1;  // last element peeled below
-            if (k0 == 0 && kend == EK) {
+            if (c > 0 && c < nc - 1) {  // interior chunk: pure recurrence
 #pragma unroll
                 for (int k = 0; k < EK; k++) {
-                    const int t = toff<T, XDIR>(lane, k);
-                    dw = step(st[t] - st[TILE + t] * dw, st[2 * TILE + t], st[3 * TILE + t]);
-                    ob[t] = dw;
+                    dw = step(rv[k] - av[k] * dw, dv[k], nv[k]);
+                    rv[k] = dw;
                 }
             } else {
-                for (int k = k0; k < kend; k++) {
-                    const int t = toff<T, XDIR>(lane, k);
-                    dw = step(st[t] - st[TILE + t] * dw, st[2 * TILE + t], st[3 * TILE + t]);
-                    ob[t] = dw;
+#pragma unroll
+                for (int k = 0; k < EK; k++) {
+                    const int e = c * EK + k;
+                    if (k < kmax) {
+                        T r = rv[k];
+                        if (e == 0) {  // folded, no recurrence term (thomas_batch dw[0])
+                            dw = step(r - av[k] * g0, dv[k], nv[k]);
+                        } else {
+                            if (e == n - 1) r = r - cl * g1;  // far ghost
+                            dw = step(r - av[k] * dw, dv[k], nv[k]);
+                        }
+                        rv[k] = dw;
+                    }
                 }
             }
-            if (c == nc - 1) {  // last element: fold the far ghost
-                const int t = toff<T, XDIR>(lane, kmax - 1);
-                const T r = st[t] - cl * g1;
-                dw = step(r - st[TILE + t] * dw, st[2 * TILE + t], st[3 * TILE + t]);
-                ob[t] = dw;
-            }
+#pragma unroll
+            for (int k = 0; k < EK; k++)
+                if (k < kmax) ob[toff<T, XDIR>(lane, k)] = rv[k];
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -195,27 +204,31 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
             __syncwarp();
             mbar_wait(&full2[s], (s_ / NS2) & 1);
             const int kmax = min(EK, n - c * EK);
-            int ktop = kmax - 1;
-            if (s_ == 0) {  // out[n-1] = dw[n-1]
-                const int t = toff<T, XDIR>(lane, ktop);
-                xv = st[t];
-                ob[t] = xv;
-                ktop--;
+            T dv[EK], cv[EK];
+#pragma unroll
+            for (int k = 0; k < EK; k++) {
+                const int t = toff<T, XDIR>(lane, k);
+                dv[k] = st[t];
+                cv[k] = st[TILE + t];
             }
-            if (ktop == EK - 1) {
+            if (s_ > 0 && kmax == EK) {
 #pragma unroll
                 for (int k = EK - 1; k >= 0; k--) {
-                    const int t = toff<T, XDIR>(lane, k);
-                    xv = st[t] - st[TILE + t] * xv;
-                    ob[t] = xv;
+                    xv = dv[k] - cv[k] * xv;
+                    dv[k] = xv;
                 }
             } else {
-                for (int k = ktop; k >= 0; k--) {
-                    const int t = toff<T, XDIR>(lane, k);
-                    xv = st[t] - st[TILE + t] * xv;
-                    ob[t] = xv;
+#pragma unroll
+                for (int k = EK - 1; k >= 0; k--) {
+                    if (k < kmax) {
+                        xv = (s_ == 0 && k == kmax - 1) ? dv[k] : dv[k] - cv[k] * xv;  // out[n-1] = dw[n-1]
+                        dv[k] = xv;
+                    }
                 }
             }
+#pragma unroll
+            for (int k = 0; k < EK; k++)
+                if (k < kmax) ob[toff<T, XDIR>(lane, k)] = dv[k];
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
