@@ -129,40 +129,38 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
             // the whole chunk goes to registers first: the ring and the out tile
             // share one smem base, so interleaved loads could not be hoisted past
             // the stores and every element would pay an LDS round trip on the chain
-            T rv[EK], av[EK], dv[EK], nv[EK];
-#pragma unroll
-            for (int k = 0; k < EK; k++) {
-                const int t = toff<T, XDIR>(lane, k);
-                rv[k] = st[t];
-                av[k] = st[TILE + t];
-                dv[k] = st[2 * TILE + t];
-                nv[k] = st[3 * TILE + t];
-            }
             if (c > 0 && c < nc - 1) {  // interior chunk: pure recurrence
+                T rv[EK], av[EK], dv[EK], nv[EK];
+#pragma unroll
+                for (int k = 0; k < EK; k++) {
+                    const int t = toff<T, XDIR>(lane, k);
+                    rv[k] = st[t];
+                    av[k] = st[TILE + t];
+                    dv[k] = st[2 * TILE + t];
+                    nv[k] = st[3 * TILE + t];
+                }
 #pragma unroll
                 for (int k = 0; k < EK; k++) {
                     dw = step(rv[k] - av[k] * dw, dv[k], nv[k]);
                     rv[k] = dw;
                 }
-            } else {
 #pragma unroll
-                for (int k = 0; k < EK; k++) {
+                for (int k = 0; k < EK; k++) ob[toff<T, XDIR>(lane, k)] = rv[k];
+            } else {  // first / last chunk of the line (2 of n/EK): fold the ghosts
+                for (int k = 0; k < kmax; k++) {
+                    const int t = toff<T, XDIR>(lane, k);
                     const int e = c * EK + k;
-                    if (k < kmax) {
-                        T r = rv[k];
-                        if (e == 0) {  // folded, no recurrence term (thomas_batch dw[0])
-                            dw = step(r - av[k] * g0, dv[k], nv[k]);
-                        } else {
-                            if (e == n - 1) r = r - cl * g1;  // far ghost
-                            dw = step(r - av[k] * dw, dv[k], nv[k]);
-                        }
-                        rv[k] = dw;
+                    T r = st[t];
+                    const T a = st[TILE + t];
+                    if (e == 0) {  // folded, no recurrence term (thomas_batch dw[0])
+                        dw = step(r - a * g0, st[2 * TILE + t], st[3 * TILE + t]);
+                    } else {
+                        if (e == n - 1) r = r - cl * g1;  // far ghost
+                        dw = step(r - a * dw, st[2 * TILE + t], st[3 * TILE + t]);
                     }
+                    ob[t] = dw;
                 }
             }
-#pragma unroll
-            for (int k = 0; k < EK; k++)
-                if (k < kmax) ob[toff<T, XDIR>(lane, k)] = rv[k];
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -204,31 +202,28 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
             __syncwarp();
             mbar_wait(&full2[s], (s_ / NS2) & 1);
             const int kmax = min(EK, n - c * EK);
-            T dv[EK], cv[EK];
+            if (s_ > 0 && kmax == EK) {  // interior chunk
+                T dv[EK], cv[EK];
 #pragma unroll
-            for (int k = 0; k < EK; k++) {
-                const int t = toff<T, XDIR>(lane, k);
-                dv[k] = st[t];
-                cv[k] = st[TILE + t];
-            }
-            if (s_ > 0 && kmax == EK) {
+                for (int k = 0; k < EK; k++) {
+                    const int t = toff<T, XDIR>(lane, k);
+                    dv[k] = st[t];
+                    cv[k] = st[TILE + t];
+                }
 #pragma unroll
                 for (int k = EK - 1; k >= 0; k--) {
                     xv = dv[k] - cv[k] * xv;
                     dv[k] = xv;
                 }
-            } else {
 #pragma unroll
-                for (int k = EK - 1; k >= 0; k--) {
-                    if (k < kmax) {
-                        xv = (s_ == 0 && k == kmax - 1) ? dv[k] : dv[k] - cv[k] * xv;  // out[n-1] = dw[n-1]
-                        dv[k] = xv;
-                    }
+                for (int k = 0; k < EK; k++) ob[toff<T, XDIR>(lane, k)] = dv[k];
+            } else {  // the line's last chunk: out[n-1] = dw[n-1]
+                for (int k = kmax - 1; k >= 0; k--) {
+                    const int t = toff<T, XDIR>(lane, k);
+                    xv = (s_ == 0 && k == kmax - 1) ? st[t] : st[t] - st[TILE + t] * xv;
+                    ob[t] = xv;
                 }
             }
-#pragma unroll
-            for (int k = 0; k < EK; k++)
-                if (k < kmax) ob[toff<T, XDIR>(lane, k)] = dv[k];
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
