@@ -80,5 +80,7 @@ void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st
 
 template void launch_correct<double>(const Consts<double> &, const CorrectPtrs<double> &,
                                      cudaStream_t);
+template void launch_correct<float>(const Consts<float> &, const CorrectPtrs<float> &,
+                                    cudaStream_t);
 
 }  // namespace bsq

@@ -225,5 +225,8 @@ template void launch_final<double>(const Consts<double> &, const FinalPtrs<doubl
                                    cudaStream_t);
 template void launch_extrema<double>(const Consts<double> &, const double *, const double *,
                                      const double *, const double *, Partial *, cudaStream_t);
+template void launch_final<float>(const Consts<float> &, const FinalPtrs<float> &, cudaStream_t);
+template void launch_extrema<float>(const Consts<float> &, const float *, const float *,
+                                    const float *, const float *, Partial *, cudaStream_t);
 
 }  // namespace bsq

@@ -94,5 +94,8 @@ void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw
 template void launch_ghost<double>(const Consts<double> &, const DevParams *, int, const double *,
                                    const double *, const double *, double *, double *, double *,
                                    cudaStream_t);
+template void launch_ghost<float>(const Consts<float> &, const DevParams *, int, const float *,
+                                  const float *, const float *, float *, float *, float *,
+                                  cudaStream_t);
 
 }  // namespace bsq

@@ -274,5 +274,7 @@ int solve_chunk_elems(int elem_bytes) { return 128 / elem_bytes; }
 
 template void launch_solve<double>(const Consts<double> &, const SolveMaps &,
                                    const SolvePtrs<double> &, bool, cudaStream_t);
+template void launch_solve<float>(const Consts<float> &, const SolveMaps &,
+                                  const SolvePtrs<float> &, bool, cudaStream_t);
 
 }  // namespace bsq

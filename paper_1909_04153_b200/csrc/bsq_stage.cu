@@ -335,5 +335,7 @@ void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A,
 
 template void launch_stage<double>(const Consts<double> &, const DevParams *,
                                    const StagePtrs<double> &, int, cudaStream_t);
+template void launch_stage<float>(const Consts<float> &, const DevParams *,
+                                  const StagePtrs<float> &, int, cudaStream_t);
 
 }  // namespace bsq

@@ -168,14 +168,16 @@ class Simulator:
     """Adaptive-AB3 Boussinesq simulation whose per-step work runs on a B200.
 
     Constructor, ``advance``/``run`` and attributes as the reference
-    (stepper.py:170-340).  Extra keyword: ``device`` (torch device spec).
+    (stepper.py:170-340).  Extra keywords: ``device`` (torch device spec) and
+    ``precision``: "fp64" (default; bitwise equal to the reference) or "fp32"
+    (device storage and arithmetic in float; host API stays float64).
     """
 
     def __init__(self, bathy, state, boundaries, controller,
                  numerics: NumericsParams | None = None, phys: PhysParams | None = None,
                  solver: str = "thomas", blowup_bound: float | None = None,
                  cross_correction: bool = True, h_dry: float | None = None,
-                 device=None):
+                 device=None, precision: str = "fp64"):
         self.bathy = bathy
         self.boundaries = boundaries
         self.controller = controller
@@ -197,9 +199,13 @@ class Simulator:
         self._kinds = [bc.policy_kind(p) for p in self._policies]
         self._warn_dominance()
 
+        if precision not in ("fp64", "fp32"):
+            raise ValueError(f"precision must be 'fp64' or 'fp32', got {precision!r}")
+        self.precision = precision
         d = nat.Desc()
         d.nx, d.ny = grid.nx, grid.ny
-        d.precision, d.solver = nat.FP64, nat.THOMAS
+        d.precision = nat.FP64 if precision == "fp64" else nat.FP32
+        d.solver = nat.THOMAS
         d.cross_correction = 1 if cross_correction else 0
         self._bands = [None] * 4
         for k, (side, pol, kind) in enumerate(zip(bc.SIDES, self._policies, self._kinds)):
@@ -267,6 +273,9 @@ class Simulator:
         hs = self._host_state
         if hs is None:
             return
+        if self._host_pristine is None:  # read-only large-grid copy: nothing to sync
+            self._host_state = None
+            return
         pw, pp, pq = self._host_pristine
         changed = any(a.shape != b.shape or (a.view(np.uint64) != b.view(np.uint64)).any()
                       for a, b in ((hs.w, pw), (hs.p, pp), (hs.q, pq)))
@@ -277,18 +286,41 @@ class Simulator:
 
     @property
     def state(self) -> FieldState:
+        """Host copy of the committed state, downloaded on first access after a
+        step.  Small grids (<= EDIT_TRACK_BYTES) keep the reference's
+        semantics that in-place edits of ``sim.state`` take effect: the edit
+        is uploaded before the next step.  Larger grids hand out read-only
+        arrays instead of paying a full host copy per access; assign
+        ``sim.state = ...`` to replace them."""
         if self._host_state is None:
             w, p, q = self._dev.download()
-            self._host_pristine = (w.copy(), p.copy(), q.copy())
+            if 3 * w.nbytes <= self.EDIT_TRACK_BYTES:
+                self._host_pristine = (w.copy(), p.copy(), q.copy())
+            else:
+                for a in (w, p, q):
+                    a.flags.writeable = False
+                self._host_pristine = None
             self._host_state = FieldState(w, p, q)
         return self._host_state
 
     @state.setter
     def state(self, new_state):
-        _validate_state(new_state, self.bathy)
+        shape = self.bathy.grid.shape_padded
+        for a in (new_state.w, new_state.p, new_state.q):
+            if a.shape != shape:
+                raise ValueError(f"state array has shape {a.shape}, expected {shape}")
         self._host_state = None
         self._host_pristine = None
         self._dev.upload(new_state.w, new_state.p, new_state.q)
+
+    EDIT_TRACK_BYTES = 64 << 20
+
+    def download_state(self, out=None) -> FieldState:
+        """Copy the committed state into ``out`` (a FieldState or (w, p, q),
+        e.g. pinned arrays) or fresh arrays, without edit tracking."""
+        arrs = None if out is None else (
+            (out.w, out.p, out.q) if hasattr(out, "w") else tuple(out))
+        return FieldState(*self._dev.download(out=arrs))
 
     def _pending_state(self) -> FieldState:
         return FieldState(*self._dev.download(pending=True))
