@@ -241,6 +241,33 @@ def main():
     del sim
     torch.cuda.empty_cache()
 
+    # ---- the fp32 mode on the same workload (extra field; the headline is fp64) ----
+    sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
+                            stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
+                            device=dev, precision="fp32")
+    for _ in range(max(args.warmup, 3)):
+        sim.advance()
+    torch.cuda.synchronize(dev)
+    s32, e32 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s32.record(sim._dev.stream)
+    for _ in range(args.steps):
+        sim.advance()
+    e32.record(sim._dev.stream)
+    torch.cuda.synchronize(dev)
+    ms32 = s32.elapsed_time(e32)
+    if dist is not None:
+        t = torch.tensor([ms32], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms32 = float(t.item())
+    v32 = cells * world * args.steps / (ms32 * 1e-3) / 1e9
+    hbm_, _ = peaks()
+    fp32 = {"value": v32, "unit": "Gcell-updates/s", "ms_per_step": ms32 / args.steps,
+            "step_frac": v32 / world * (B_ALG_STEP // 2) / hbm_,
+            "parity": "eta rel-L2 <= 1e-4, wet/dry mask exact (tests/test_gpu_fp32.py)"}
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
+
     hbm, peak_kind = peaks()
     avg = {k: float(np.mean(v)) for k, v in per_kernel.items()}
     dom = max((k for k in avg if k in KERNEL_BYTES and KERNEL_BYTES[k] > 0), key=lambda k: avg[k])
@@ -304,7 +331,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (rip-channel bathymetry, JONSWAP maker; reference generators)",
             "config": config_dict(args, case), "roofline": roofline, "cpu_baseline": cpu,
-            "e2e": e2e, "gpu_launches": kps * args.steps, "clocks": clock_info,
+            "e2e": e2e, "gpu_launches": kps * args.steps, "clocks": clock_info, "fp32": fp32,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
