@@ -63,13 +63,22 @@ typedef struct {
     int32_t sponge_len[4];     /* band length, 0 = none */
     double dx, dy, dx2, dy2;
     double g, b_disp, bp13, c_f, theta, h_eps, h_dry, ws;
+    /* y-strip sharding (one context per rank; all zero for a whole grid).
+     * The context holds interior rows [row0, row0+ny) of a global grid; an
+     * internal side has no boundary policy: its two ghost rows are the
+     * neighbour's interior rows, exchanged by the host between phases. */
+    int32_t south_internal, north_internal;
+    int32_t row0, ny_global;
 } bsq_desc;
 
-/* Static fields (host pointers, reference layout; copied at create). */
+/* Static fields (host pointers, reference layout; copied at create).  For a
+ * strip, rows are the strip's interior plus 2 rows of the global array on
+ * each side (bed_face_y: ny+3 rows starting at the strip's padded row 0). */
 typedef struct {
     const double *bed_eff, *depth, *depth_dx, *depth_dy; /* (ny+4) x (nx+4) */
     const double *bed_face_x;                            /* (ny+4) x (nx+3) */
     const double *bed_face_y;                            /* (ny+3) x (nx+4) */
+    const double *cw_south; /* strip with internal south: cw of the row below, per column (nx) */
 } bsq_static;
 
 /* Per-step host scalars (stepper.py:239-254; multistep.py:118-228;
@@ -130,6 +139,43 @@ int bsq_solve_momentum(bsq_ctx *ctx, const double *ustar, const double *vstar,
 int bsq_speed_extrema(bsq_ctx *ctx, double *out3);
 /* Boundaries.apply_ghosts on the committed state with maker values */
 int bsq_fill_ghosts(bsq_ctx *ctx, const double *maker_eta, const double *maker_flux);
+
+/* -- y-strip sharding: phased step and device layout ------------------------ */
+/* A sharded step is bsq_step split at its exchange points; the host moves
+ * halo rows and the y-line boundary vectors between phases on the context's
+ * stream (NCCL send/recv, or device copies when ranks are emulated):
+ *   BSQ_PH_GHOST   upload params, ghost strips at t (physical sides only)
+ *     -> exchange 2 rows of w, P, Q with each neighbour
+ *   BSQ_PH_STAGE   stage kernel + predicted-state ghosts at t+dt
+ *   BSQ_PH_SOLVE1F x lines (complete) + y lines forward sweep
+ *     (needs dw_in from the south rank; produces dw_out for the north rank)
+ *   BSQ_PH_SOLVE1B y lines back substitution (x_in from the north rank;
+ *     produces x_out for the south rank)
+ *     -> exchange 1 row of the pending P, Q with each neighbour
+ *   BSQ_PH_CORRECT cross-correction right-hand sides
+ *   BSQ_PH_SOLVE2F, BSQ_PH_SOLVE2B  second solve, as above
+ *   BSQ_PH_FINAL   finalize + reductions -> result (local; the host reduces
+ *                  across ranks), synchronizes the stream */
+enum {
+    BSQ_PH_GHOST = 0, BSQ_PH_STAGE = 1, BSQ_PH_SOLVE1F = 2, BSQ_PH_SOLVE1B = 3,
+    BSQ_PH_CORRECT = 4, BSQ_PH_SOLVE2F = 5, BSQ_PH_SOLVE2B = 6, BSQ_PH_FINAL = 7
+};
+int bsq_phase(bsq_ctx *ctx, int phase, const bsq_step_params *params, bsq_step_result *result);
+/* cw of this strip's last row, per column (nx): the next strip's cw_south */
+int bsq_factor_tail(bsq_ctx *ctx, double *cw_north);
+/* Device placement of a named array inside the workspace (byte offset from
+ * the workspace base, row pitch and padded-column offset in elements, element
+ * size).  The committed/pending state buffers swap every commit. */
+enum {
+    BSQ_ARR_W = 0, BSQ_ARR_P = 1, BSQ_ARR_Q = 2,                /* committed state */
+    BSQ_ARR_W_NEW = 3, BSQ_ARR_P_NEW = 4, BSQ_ARR_Q_NEW = 5,    /* pending state */
+    BSQ_ARR_DW_IN = 6, BSQ_ARR_DW_OUT = 7, BSQ_ARR_X_IN = 8, BSQ_ARR_X_OUT = 9 /* nx vectors */
+};
+int bsq_array_layout(bsq_ctx *ctx, int array, size_t *byte_offset, int *pitch, int *xo,
+                     int *elem_bytes);
+/* whether every Thomas pivot of this context is > 0, and whether one is 0
+ * (a sharded run raises if any rank is singular) */
+int bsq_pivot_flags(bsq_ctx *ctx, int *all_positive, int *singular);
 
 /* -- timing support ------------------------------------------------------ */
 /* When enabled, bsq_step brackets each kernel with CUDA events on the

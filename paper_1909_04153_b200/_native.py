@@ -30,12 +30,20 @@ class Desc(ctypes.Structure):
                 ("dx2", ctypes.c_double), ("dy2", ctypes.c_double),
                 ("g", ctypes.c_double), ("b_disp", ctypes.c_double), ("bp13", ctypes.c_double),
                 ("c_f", ctypes.c_double), ("theta", ctypes.c_double), ("h_eps", ctypes.c_double),
-                ("h_dry", ctypes.c_double), ("ws", ctypes.c_double)]
+                ("h_dry", ctypes.c_double), ("ws", ctypes.c_double),
+                ("south_internal", ctypes.c_int32), ("north_internal", ctypes.c_int32),
+                ("row0", ctypes.c_int32), ("ny_global", ctypes.c_int32)]
 
 
 class Static(ctypes.Structure):
     _fields_ = [("bed_eff", _dp), ("depth", _dp), ("depth_dx", _dp), ("depth_dy", _dp),
-                ("bed_face_x", _dp), ("bed_face_y", _dp)]
+                ("bed_face_x", _dp), ("bed_face_y", _dp), ("cw_south", _dp)]
+
+
+# phased step (y-strip sharding) and device array ids -- include/bsq.h
+PH_GHOST, PH_STAGE, PH_SOLVE1F, PH_SOLVE1B, PH_CORRECT, PH_SOLVE2F, PH_SOLVE2B, PH_FINAL = range(8)
+ARR_W, ARR_P, ARR_Q, ARR_W_NEW, ARR_P_NEW, ARR_Q_NEW, ARR_DW_IN, ARR_DW_OUT, ARR_X_IN, ARR_X_OUT = \
+    range(10)
 
 
 class StepParams(ctypes.Structure):
@@ -79,6 +87,15 @@ SIGNATURES = [
                                         ctypes.POINTER(ctypes.c_char_p),
                                         ctypes.POINTER(ctypes.c_int)]),
     ("bsq_kernels_per_step", ctypes.c_int, [ctypes.c_void_p]),
+    ("bsq_phase", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(StepParams),
+                                 ctypes.POINTER(StepResult)]),
+    ("bsq_factor_tail", ctypes.c_int, [ctypes.c_void_p, _dp]),
+    ("bsq_array_layout", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_size_t),
+                                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(ctypes.c_int)]),
+    ("bsq_pivot_flags", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
+                                       ctypes.POINTER(ctypes.c_int)]),
 ]
 
 _lib = None

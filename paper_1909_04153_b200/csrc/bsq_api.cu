@@ -49,7 +49,8 @@ enum Arr {
     A_COUNT = A_HIST0 + 20
 };
 
-enum Small { S_CXL, S_CYL, S_FAC, S_PAR, S_RES, S_PART, S_CNT, S_COUNT };
+enum Small { S_CXL, S_CYL, S_FAC, S_PAR, S_RES, S_PART, S_CNT, S_DWIN, S_DWOUT, S_XIN, S_XOUT,
+             S_COUNT };
 
 template <class T>
 Layout make_layout(const bsq_desc *d) {
@@ -76,7 +77,9 @@ size_t layout_bytes(const bsq_desc *d, size_t offs[A_COUNT + S_COUNT], int *fac_
     *fac_stride = fs;
     const size_t small[S_COUNT] = {sizeof(T) * d->ny, sizeof(T) * d->nx, sizeof(T) * 4 * fs,
                                    sizeof(DevParams), sizeof(DevResult),
-                                   sizeof(Partial) * (size_t)final_blocks(d->nx, d->ny), 256};
+                                   sizeof(Partial) * (size_t)final_blocks(d->nx, d->ny), 256,
+                                   sizeof(T) * d->nx, sizeof(T) * d->nx, sizeof(T) * d->nx,
+                                   sizeof(T) * d->nx};
     for (int k = 0; k < S_COUNT; k++) {
         offs[A_COUNT + k] = off;
         off += align256(small[k]);
@@ -91,6 +94,13 @@ int check_desc(const bsq_desc *d) {
         return fail(BSQ_ERR_BAD_ARG, "precision must be BSQ_FP64 or BSQ_FP32");
     if (d->solver != BSQ_THOMAS) return fail(BSQ_ERR_BAD_ARG, "only the Thomas solver is built");
     if (!(d->dx > 0 && d->dy > 0)) return fail(BSQ_ERR_BAD_ARG, "cell sizes must be positive");
+    if (d->south_internal || d->north_internal) {
+        if (d->row0 < 0 || d->row0 + d->ny > d->ny_global)
+            return fail(BSQ_ERR_BAD_ARG, "strip rows outside the global grid");
+        if ((d->south_internal != 0) != (d->row0 > 0) ||
+            (d->north_internal != 0) != (d->row0 + d->ny < d->ny_global))
+            return fail(BSQ_ERR_BAD_ARG, "internal sides must face other strips");
+    }
     for (int s = 0; s < 4; s++) {
         if (d->side_kind[s] < 0 || d->side_kind[s] > 2) return fail(BSQ_ERR_BAD_ARG, "bad side kind");
         const int n = (s == SIDE_E || s == SIDE_W) ? d->nx : d->ny;
@@ -142,6 +152,10 @@ struct Engine : EngineBase {
     bool own_stream = false;
     T *arr[A_COUNT];
     T *cx_last = nullptr, *cy_last = nullptr, *fac[4];
+    T *dw_in = nullptr, *dw_out = nullptr, *x_in = nullptr, *x_out = nullptr;  // strip boundaries
+    std::vector<double> cw_tail;   // cw of the strip's last row per column (next strip's cw_south)
+    size_t offs[A_COUNT + S_COUNT];
+    char *base = nullptr;
     DevParams *dparams = nullptr;
     DevResult *dres = nullptr;
     Partial *part = nullptr;
@@ -158,7 +172,7 @@ struct Engine : EngineBase {
     int nev = 0, last_n = 0;
     float last_ms[kMaxEv] = {};
     SolveMaps maps;                  // TMA descriptors (out slots patched per launch)
-    CUtensorMap x_out[3], y_out[3];  // pending P/Q of state 0, state 1; P2/Q2
+    CUtensorMap map_xout[3], map_yout[3];  // pending P/Q of state 0, state 1; P2/Q2
 
     T *W(int s) { return arr[s ? A_W1 : A_W0]; }
     T *Pp(int s) { return arr[s ? A_P1 : A_P0]; }
@@ -253,6 +267,8 @@ struct Engine : EngineBase {
             C.sponge_lo[s] = p->sponge_lo[s];
             C.sponge_len[s] = p->sponge_len[s];
         }
+        if (p->south_internal) C.side_kind[SIDE_S] = KIND_INTERNAL;
+        if (p->north_internal) C.side_kind[SIDE_N] = KIND_INTERNAL;
         C.cross = p->cross_correction;
     }
 
@@ -291,18 +307,25 @@ struct Engine : EngineBase {
                 if (i == nx - 1) cxl[j] = T(cc);
             }
         }
-        for (int i = 0; i < nx; i++) {  // y columns
-            double cw_prev = 0.0;
+        // y columns; a strip with an internal south side continues the global
+        // column's recurrence from the south strip's last cw
+        if (d.south_internal && !f->cw_south)
+            return fail(BSQ_ERR_BAD_ARG, "strip with an internal south side needs cw_south");
+        cw_tail.assign(nx, 0.0);
+        for (int i = 0; i < nx; i++) {
+            const bool cont = d.south_internal != 0;
+            double cw_prev = cont ? f->cw_south[i] : 0.0;
             for (int j = 0; j < ny; j++) {
                 const long h = (long)(j + GL) * nxt + i + GL;
                 double a, b, cc;
                 coefficients(f->depth[h], f->depth_dy[h], d.dy2, six_dy, d.bp13, &a, &b, &cc);
-                const double den = j == 0 ? b : b - a * cw_prev;
+                const double den = (j == 0 && !cont) ? b : b - a * cw_prev;
                 const double cw = cc / den;
                 put(ay, deny, rdeny, cwy, L.at(j + GL, i + GL), a, den, cw);
                 cw_prev = cw;
                 if (j == ny - 1) cyl[i] = T(cc);
             }
+            cw_tail[i] = cw_prev;
         }
         singular = sing;
         pos_pivots = pos;
@@ -345,10 +368,10 @@ struct Engine : EngineBase {
             (rc = make_map(&M.y_rhs, arr[A_VS], false)) || (rc = make_map(&M.y_a, arr[A_AY], false)) ||
             (rc = make_map(&M.y_den, arr[A_DENY], false)) ||
             (rc = make_map(&M.y_rden, arr[A_RDENY], false)) ||
-            (rc = make_map(&M.y_cw, arr[A_CWY], false)) || (rc = make_map(&x_out[0], Pp(0), true)) ||
-            (rc = make_map(&x_out[1], Pp(1), true)) || (rc = make_map(&x_out[2], arr[A_P2], true)) ||
-            (rc = make_map(&y_out[0], Qq(0), false)) || (rc = make_map(&y_out[1], Qq(1), false)) ||
-            (rc = make_map(&y_out[2], arr[A_Q2], false)))
+            (rc = make_map(&M.y_cw, arr[A_CWY], false)) || (rc = make_map(&map_xout[0], Pp(0), true)) ||
+            (rc = make_map(&map_xout[1], Pp(1), true)) || (rc = make_map(&map_xout[2], arr[A_P2], true)) ||
+            (rc = make_map(&map_yout[0], Qq(0), false)) || (rc = make_map(&map_yout[1], Qq(1), false)) ||
+            (rc = make_map(&map_yout[2], arr[A_Q2], false)))
             return rc;
         return BSQ_OK;
     }
@@ -356,13 +379,16 @@ struct Engine : EngineBase {
     int create(const bsq_desc *desc, const bsq_static *f, void *workspace, size_t bytes, void *stream) {
         d = *desc;
         L = make_layout<T>(desc);
-        size_t offs[A_COUNT + S_COUNT];
         const size_t need = layout_bytes<T>(desc, offs, &fac_stride);
         if (bytes < need) return fail(BSQ_ERR_BAD_ARG, "workspace too small");
         if (((uintptr_t)workspace & 255) != 0) return fail(BSQ_ERR_BAD_ARG, "workspace not 256-B aligned");
         nfinal = final_blocks(desc->nx, desc->ny);
-        char *base = (char *)workspace;
+        base = (char *)workspace;
         for (int k = 0; k < A_COUNT; k++) arr[k] = (T *)(base + offs[k]);
+        dw_in = (T *)(base + offs[A_COUNT + S_DWIN]);
+        dw_out = (T *)(base + offs[A_COUNT + S_DWOUT]);
+        x_in = (T *)(base + offs[A_COUNT + S_XIN]);
+        x_out = (T *)(base + offs[A_COUNT + S_XOUT]);
         cx_last = (T *)(base + offs[A_COUNT + S_CXL]);
         cy_last = (T *)(base + offs[A_COUNT + S_CYL]);
         for (int s = 0; s < 4; s++) fac[s] = (T *)(base + offs[A_COUNT + S_FAC]) + s * fac_stride;
@@ -458,7 +484,7 @@ struct Engine : EngineBase {
         bool any = false;
         for (int s = 0; s < 4; s++) {
             const int n = d.sponge_len[s];
-            if (d.side_kind[s] == BSQ_SPONGE && n > 0) {
+            if (n > 0) {
                 if (!p->sponge_fac[s]) return fail(BSQ_ERR_BAD_ARG, "missing sponge factors");
                 T *dst = hfac + (size_t)s * fac_stride;
                 for (int k = 0; k < n; k++) dst[k] = T(p->sponge_fac[s][k]);
@@ -503,6 +529,12 @@ struct Engine : EngineBase {
         S.gq = Qq(nxt_state);
         S.cx_last = cx_last;
         S.cy_last = cy_last;
+        S.south_int = d.south_internal;
+        S.north_int = d.north_internal;
+        S.dw_in = dw_in;
+        S.dw_out = dw_out;
+        S.x_in = x_in;
+        S.x_out = x_out;
         return S;
     }
 
@@ -510,8 +542,8 @@ struct Engine : EngineBase {
     // corrected right-hand sides (written over us / vs) into P2, Q2
     const SolveMaps &solve_maps(int phase, int nxt_state) {
         const int k = phase == 1 ? nxt_state : 2;
-        maps.x_out = x_out[k];
-        maps.y_out = y_out[k];
+        maps.x_out = map_xout[k];
+        maps.y_out = map_yout[k];
         return maps;
     }
 
@@ -542,28 +574,78 @@ struct Engine : EngineBase {
         for (int k = 0; k < 3; k++) r->state_bad[k] = h.state_bad[k] == ~0ull ? -1 : (int64_t)h.state_bad[k];
     }
 
-    int step(const bsq_step_params *p, bsq_step_result *r) {
-        int rc = stage_params(p);
-        if (rc) return rc;
-        CU(cudaMemsetAsync(dres, 0xFF, sizeof(DevResult), st));
+    bool strip() const { return d.south_internal || d.north_internal; }
+
+    // One phase of the step (include/bsq.h BSQ_PH_*).  For a whole grid the
+    // y-line solves run complete inside the *F phases and the *B phases are
+    // empty; for a strip they split at the rank boundary exchange.
+    int phase(int ph, const bsq_step_params *p, bsq_step_result *r) {
         const int nxt = 1 - cur;
         const int slot = (head + 1) % 4;
-        nev = 0;
-        ev_mark("start");
-        launch_ghost(C, dparams, 0, W(cur), Pp(cur), Qq(cur), W(cur), Pp(cur), Qq(cur), st);
-        ev_mark("ghost_t");
-        launch_stage(C, dparams, stage_ptrs(slot), 1, st);
-        ev_mark("stage");
-        launch_ghost(C, dparams, 1, W(nxt), Pp(cur), Qq(cur), W(nxt), Pp(nxt), Qq(nxt), st);
-        ev_mark("ghost_n");
-        launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st);
-        ev_mark("solve1");
-        if (d.cross_correction) {
-            launch_correct(C, correct_ptrs(slot, nxt), st);
-            ev_mark("correct");
-            launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st);
-            ev_mark("solve2");
+        const int fwd_mode = strip() ? SOLVE_X_YFWD : SOLVE_FULL;
+        switch (ph) {
+        case BSQ_PH_GHOST: {
+            int rc = stage_params(p);
+            if (rc) return rc;
+            CU(cudaMemsetAsync(dres, 0xFF, sizeof(DevResult), st));
+            nev = 0;
+            ev_mark("start");
+            launch_ghost(C, dparams, 0, W(cur), Pp(cur), Qq(cur), W(cur), Pp(cur), Qq(cur), st);
+            ev_mark("ghost_t");
+            break;
         }
+        case BSQ_PH_STAGE:
+            launch_stage(C, dparams, stage_ptrs(slot), 1, st);
+            ev_mark("stage");
+            launch_ghost(C, dparams, 1, W(nxt), Pp(cur), Qq(cur), W(nxt), Pp(nxt), Qq(nxt), st);
+            ev_mark("ghost_n");
+            break;
+        case BSQ_PH_SOLVE1F:
+            launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st, fwd_mode);
+            ev_mark("solve1");
+            break;
+        case BSQ_PH_SOLVE1B:
+            if (strip()) {
+                launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st, SOLVE_YBWD);
+                ev_mark("solve1b");
+            }
+            break;
+        case BSQ_PH_CORRECT:
+            if (d.cross_correction) {
+                launch_correct(C, correct_ptrs(slot, nxt), st);
+                ev_mark("correct");
+            }
+            break;
+        case BSQ_PH_SOLVE2F:
+            if (d.cross_correction) {
+                launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st, fwd_mode);
+                ev_mark("solve2");
+            }
+            break;
+        case BSQ_PH_SOLVE2B:
+            if (d.cross_correction && strip()) {
+                launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st, SOLVE_YBWD);
+                ev_mark("solve2b");
+            }
+            break;
+        case BSQ_PH_FINAL:
+            return finish(r, slot, nxt);
+        default:
+            return fail(BSQ_ERR_BAD_ARG, "unknown phase");
+        }
+        CU(cudaGetLastError());
+        return BSQ_OK;
+    }
+
+    int step(const bsq_step_params *p, bsq_step_result *r) {
+        for (int ph = BSQ_PH_GHOST; ph <= BSQ_PH_FINAL; ph++) {
+            const int rc = phase(ph, p, r);
+            if (rc) return rc;
+        }
+        return BSQ_OK;
+    }
+
+    int finish(bsq_step_result *r, int slot, int nxt) {
         FinalPtrs<T> F;
         F.w = W(nxt);
         F.pin = d.cross_correction ? arr[A_P2] : Pp(nxt);
@@ -590,6 +672,28 @@ struct Engine : EngineBase {
         bool stage_err = false;
         for (int k = 0; k < 5; k++) stage_err |= r->stage_bad[k] >= 0;
         if (singular && !stage_err) return fail(BSQ_ERR_SINGULAR, "singular tridiagonal system: zero pivot");
+        return BSQ_OK;
+    }
+
+    int array_layout(int which, size_t *off, int *pitch, int *xo, int *eb) {
+        const T *ptr = nullptr;
+        switch (which) {
+        case BSQ_ARR_W: ptr = W(cur); break;
+        case BSQ_ARR_P: ptr = Pp(cur); break;
+        case BSQ_ARR_Q: ptr = Qq(cur); break;
+        case BSQ_ARR_W_NEW: ptr = W(1 - cur); break;
+        case BSQ_ARR_P_NEW: ptr = Pp(1 - cur); break;
+        case BSQ_ARR_Q_NEW: ptr = Qq(1 - cur); break;
+        case BSQ_ARR_DW_IN: ptr = dw_in; break;
+        case BSQ_ARR_DW_OUT: ptr = dw_out; break;
+        case BSQ_ARR_X_IN: ptr = x_in; break;
+        case BSQ_ARR_X_OUT: ptr = x_out; break;
+        default: return fail(BSQ_ERR_BAD_ARG, "unknown array id");
+        }
+        *off = (size_t)((const char *)ptr - base);
+        *pitch = L.pitch;
+        *xo = L.xo;
+        *eb = (int)sizeof(T);
         return BSQ_OK;
     }
 
@@ -762,6 +866,31 @@ int bsq_step(bsq_ctx *c, const bsq_step_params *p, bsq_step_result *r) {
 int bsq_commit(bsq_ctx *c) {
     if (!c) return fail(BSQ_ERR_BAD_ARG, "null ctx");
     return ENGINE(c, e->commit());
+}
+
+int bsq_phase(bsq_ctx *c, int phase, const bsq_step_params *p, bsq_step_result *r) {
+    if (!c || (phase == BSQ_PH_GHOST && !p) || (phase == BSQ_PH_FINAL && !r))
+        return fail(BSQ_ERR_BAD_ARG, "null argument");
+    return ENGINE(c, e->phase(phase, p, r));
+}
+
+int bsq_factor_tail(bsq_ctx *c, double *cw_north) {
+    if (!c || !cw_north) return fail(BSQ_ERR_BAD_ARG, "null argument");
+    return ENGINE(c, ([&] {
+        for (size_t k = 0; k < e->cw_tail.size(); k++) cw_north[k] = e->cw_tail[k];
+        return (int)BSQ_OK;
+    })());
+}
+
+int bsq_array_layout(bsq_ctx *c, int array, size_t *off, int *pitch, int *xo, int *eb) {
+    if (!c || !off || !pitch || !xo || !eb) return fail(BSQ_ERR_BAD_ARG, "null argument");
+    return ENGINE(c, e->array_layout(array, off, pitch, xo, eb));
+}
+
+int bsq_pivot_flags(bsq_ctx *c, int *all_positive, int *singular) {
+    if (!c || !all_positive || !singular) return fail(BSQ_ERR_BAD_ARG, "null argument");
+    return ENGINE(c, (*all_positive = e->pos_pivots ? 1 : 0, *singular = e->singular ? 1 : 0,
+                      (int)BSQ_OK));
 }
 
 int bsq_stage_rates(bsq_ctx *c, double *e_, double *f, double *g, double *fs, double *gs) {

@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(FT) k_final(Consts<T> C, FinalPtrs<T> F) {
         const T rest = C.ws > be ? C.ws : be;  // np.maximum(ws, bed_eff)
 #pragma unroll
         for (int side = 0; side < 4; side++) {  // sponge bands, order N, S, E, W
-            if (C.side_kind[side] != KIND_SPONGE || C.sponge_len[side] == 0) continue;
+            // band in local coordinates (a strip may hold part of a N/S band)
+            if (C.sponge_len[side] == 0) continue;
             const int kk = (side == SIDE_E || side == SIDE_W) ? (I - GL) - C.sponge_lo[side]
                                                               : (J - GL) - C.sponge_lo[side];
             if (kk < 0 || kk >= C.sponge_len[side]) continue;

@@ -57,6 +57,8 @@ __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which,
         int I = c < 2 ? c : nxt - 4 + c;
         int side = c < 2 ? SIDE_W : SIDE_E;
         bool interior_row = J >= GL && J < nyt - GL;
+        // a strip's halo rows (internal N/S side) belong to the neighbour rank
+        if (!interior_row && C.side_kind[J < GL ? SIDE_S : SIDE_N] == KIND_INTERNAL) return;
         if (C.side_kind[side] == KIND_MAKER) {
             double gw = which ? P->gw_n[side] : P->gw_t[side];
             double gf = which ? P->gf_n[side] : P->gf_t[side];
@@ -79,6 +81,7 @@ __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which,
         int I = GL + (k >> 2);
         int r = k & 3;
         int J = r < 2 ? r : nyt - 4 + r;
+        if (C.side_kind[J < GL ? SIDE_S : SIDE_N] == KIND_INTERNAL) return;
 #pragma unroll
         for (int f = 0; f < 3; f++) dst[f][C.L.at(J, I)] = ns_value(C, P, which, f, J, I, src[f]);
     }

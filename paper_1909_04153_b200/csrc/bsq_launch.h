@@ -23,7 +23,16 @@ template <class T>
 struct SolvePtrs {
     const T *gp, *gq;               // arrays holding the P / Q ghost values to fold
     const T *cx_last, *cy_last;     // c_{n-1} of every x / y line (ghost folding)
+    // y-strip sharding: the y lines continue across ranks (exact pipelined Thomas)
+    int south_int, north_int;       // internal sides: no folding there
+    const T *dw_in;                 // forward: dw of the row below (south rank), per column
+    T *dw_out;                      // forward: dw of this strip's last row
+    const T *x_in;                  // backward: x of the row above (north rank)
+    T *x_out;                       // backward: x of this strip's first row
 };
+
+// which parts of the line solves a launch runs
+enum SolveMode { SOLVE_FULL = 0, SOLVE_X_YFWD = 1, SOLVE_YBWD = 2 };
 
 // TMA descriptors of the solve's operands, interior region of each pitched
 // array.  x maps: box {EK, 32} (elements along x, 32 rows), 128-B swizzle;
@@ -62,7 +71,7 @@ void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A,
                   cudaStream_t st);
 template <class T>
 void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, bool pos_pivots,
-                  cudaStream_t st);
+                  cudaStream_t st, int mode = SOLVE_FULL);
 int solve_chunk_elems(int elem_bytes);
 template <class T>
 void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st);

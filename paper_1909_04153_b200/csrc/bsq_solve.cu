@@ -55,9 +55,15 @@ __device__ __forceinline__ int toff(int ln, int k) {
     return k * NLINE + ln;  // box {32, EK}: row = element
 }
 
+// mode (y lines only; x lines always run complete): SOLVE_FULL, SOLVE_X_YFWD
+// (forward sweep only: dw stays in the output array, the strip's last dw goes
+// to dw_out) or SOLVE_YBWD (back substitution only).  For a y-strip with an
+// internal south side the first element continues the recurrence from dw_in
+// instead of folding a ghost; with an internal north side the last element
+// is not folded and the back substitution starts from x_in.
 template <class T, bool XDIR, bool POS>
 __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
-                                int line0, unsigned char *smem) {
+                                int line0, unsigned char *smem, int mode) {
     using G = TileGeom<T>;
     constexpr int EK = G::EK, TILE = G::TILE;
     const Layout L = C.L;
@@ -65,6 +71,8 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
     const int nlines = XDIR ? L.ny : L.nx;
     const int nc = (n + EK - 1) / EK;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool sint = !XDIR && S.south_int, nint = !XDIR && S.north_int;
+    if (XDIR) mode = SOLVE_FULL;
 
     T *ring = reinterpret_cast<T *>(smem);                    // NS x {r, a, den, rden}
     T *outb = reinterpret_cast<T *>(smem + G::RING_B);        // 2 out tiles
@@ -91,7 +99,9 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
     __syncthreads();
 
     // ---- forward sweep --------------------------------------------------------
-    if (warp == 1) {
+    if (mode == SOLVE_YBWD) {
+        // back substitution only
+    } else if (warp == 1) {
         if (lane == 0) {
             for (int c = 0; c < nc; c++) {
                 const int s = c % NS;
@@ -109,10 +119,16 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
     } else {
         const int line = line0 + lane;
         const bool lv = line < nlines;
-        // ghost values folded into the first/last element (implicit.py:178-179, :190-191)
-        const T g0 = !lv ? T(0) : XDIR ? S.gp[L.at(GL + line, GL - 1)] : S.gq[L.at(GL - 1, GL + line)];
-        const T g1 = !lv ? T(0) : XDIR ? S.gp[L.at(GL + line, n + GL)] : S.gq[L.at(n + GL, GL + line)];
-        const T cl = !lv ? T(0) : XDIR ? S.cx_last[line] : S.cy_last[line];
+        // ghost values folded into the first/last element (implicit.py:178-179,
+        // :190-191).  The first element computes dw0 = (r0 - a0 * g0) / den0:
+        // with an internal south side g0 is the south rank's last dw, which
+        // makes it the ordinary recurrence step of the global column.
+        const T g0 = !lv ? T(0)
+                     : XDIR ? S.gp[L.at(GL + line, GL - 1)]
+                     : sint ? S.dw_in[line]
+                            : S.gq[L.at(GL - 1, GL + line)];
+        const T g1 = (!lv || nint) ? T(0) : XDIR ? S.gp[L.at(GL + line, n + GL)] : S.gq[L.at(n + GL, GL + line)];
+        const T cl = (!lv || nint) ? T(0) : XDIR ? S.cx_last[line] : S.cy_last[line];
         // dw_i = (r_i - a_i dw_{i-1}) / den_i; the ring holds nr = -RN(1/den)
         auto step = [&](T num, T den, T nr) -> T {
             return POS ? div_static_pos(num, den, nr) : div_static(num, den, -nr);
@@ -171,6 +187,7 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                 bulk_commit();
             }
         }
+        if (nint && lv) S.dw_out[line] = dw;  // the north rank continues from here
         if (lane == 0) {
             bulk_wait_all();  // dw globally written before the backward loads read it
             fence_async_global();
@@ -179,7 +196,9 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
     __syncthreads();
 
     // ---- back substitution (chunks in reverse) -----------------------------------
-    if (warp == 1) {
+    if (mode == SOLVE_X_YFWD) {
+        // forward sweep only
+    } else if (warp == 1) {
         if (lane == 0) {
             for (int s_ = 0; s_ < nc; s_++) {
                 const int c = nc - 1 - s_, s = s_ % NS2;
@@ -193,6 +212,10 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
             }
         }
     } else {
+        const int line = line0 + lane;
+        const bool lv = line < nlines;
+        // x of the row above this strip (north rank), or none for a physical side
+        const T xn = (nint && lv) ? S.x_in[line] : T(0);
         T xv = T(0);
         for (int s_ = 0; s_ < nc; s_++) {
             const int c = nc - 1 - s_, s = s_ % NS2;
@@ -217,10 +240,13 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                 }
 #pragma unroll
                 for (int k = 0; k < EK; k++) ob[toff<T, XDIR>(lane, k)] = dv[k];
-            } else {  // the line's last chunk: out[n-1] = dw[n-1]
+            } else {  // the line's last chunk: out[n-1] = dw[n-1] (or continues from x_in)
                 for (int k = kmax - 1; k >= 0; k--) {
                     const int t = toff<T, XDIR>(lane, k);
-                    xv = (s_ == 0 && k == kmax - 1) ? st[t] : st[t] - st[TILE + t] * xv;
+                    if (s_ == 0 && k == kmax - 1)
+                        xv = nint ? st[t] - st[TILE + t] * xn : st[t];
+                    else
+                        xv = st[t] - st[TILE + t] * xv;
                     ob[t] = xv;
                 }
             }
@@ -234,6 +260,7 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                 bulk_commit();
             }
         }
+        if (sint && lv) S.x_out[line] = xv;  // the south rank continues from here
         if (lane == 0) bulk_wait_all();
     }
 }
@@ -241,21 +268,22 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
 // Blocks [0, nbx) take x lines (rows -> P); blocks [nbx, ...) y lines (columns -> Q).
 template <class T, bool POS>
 __global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_constant__ SolveMaps M,
-                                                  SolvePtrs<T> S, int nbx) {
+                                                  SolvePtrs<T> S, int nbx, int mode) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     if ((int)blockIdx.x < nbx)
-        solve_lines_tma<T, true, POS>(C, M, S, blockIdx.x * NLINE, smem);
+        solve_lines_tma<T, true, POS>(C, M, S, blockIdx.x * NLINE, smem, mode);
     else
-        solve_lines_tma<T, false, POS>(C, M, S, (blockIdx.x - nbx) * NLINE, smem);
+        solve_lines_tma<T, false, POS>(C, M, S, (blockIdx.x - nbx) * NLINE, smem, mode);
 }
 
 // pos_pivots: every Thomas pivot of both operators is > 0 (host-checked), which
 // enables the select-free quotient on the recurrence's critical path.
+// mode SOLVE_YBWD launches only the y-line CTAs.
 template <class T>
 void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, bool pos_pivots,
-                  cudaStream_t st) {
+                  cudaStream_t st, int mode) {
     const int nbx = (C.L.ny + NLINE - 1) / NLINE, nby = (C.L.nx + NLINE - 1) / NLINE;
     const int smem = TileGeom<T>::SMEM_B;
     static bool attr_set = false;
@@ -264,17 +292,18 @@ void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
         cudaFuncSetAttribute(k_solve_tma<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
+    const int bx = mode == SOLVE_YBWD ? 0 : nbx;  // x-line CTAs in this launch
     if (pos_pivots)
-        k_solve_tma<T, true><<<nbx + nby, 64, smem, st>>>(C, M, S, nbx);
+        k_solve_tma<T, true><<<bx + nby, 64, smem, st>>>(C, M, S, bx, mode);
     else
-        k_solve_tma<T, false><<<nbx + nby, 64, smem, st>>>(C, M, S, nbx);
+        k_solve_tma<T, false><<<bx + nby, 64, smem, st>>>(C, M, S, bx, mode);
 }
 
 int solve_chunk_elems(int elem_bytes) { return 128 / elem_bytes; }
 
 template void launch_solve<double>(const Consts<double> &, const SolveMaps &,
-                                   const SolvePtrs<double> &, bool, cudaStream_t);
+                                   const SolvePtrs<double> &, bool, cudaStream_t, int);
 template void launch_solve<float>(const Consts<float> &, const SolveMaps &,
-                                  const SolvePtrs<float> &, bool, cudaStream_t);
+                                  const SolvePtrs<float> &, bool, cudaStream_t, int);
 
 }  // namespace bsq

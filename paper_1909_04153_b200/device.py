@@ -27,7 +27,7 @@ class DeviceStep:
     static fields in the reference layout.
     """
 
-    def __init__(self, desc: "nat.Desc", bathy, device=None):
+    def __init__(self, desc: "nat.Desc", bathy, device=None, stream=None, cw_south=None):
         L = nat.lib()
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 step needs a CUDA device (no CPU fallback)")
@@ -41,10 +41,12 @@ class DeviceStep:
         self.nbytes = int(nbytes)
         with torch.cuda.device(self.device):
             self.workspace = torch.empty(self.nbytes, dtype=torch.uint8, device=self.device)
-            self.stream = torch.cuda.Stream(self.device)
+            self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
         self._static = [_f64(a) for a in (bathy.bed_eff, bathy.depth, bathy.depth_dx,
                                           bathy.depth_dy, bathy.bed_face_x, bathy.bed_face_y)]
-        st = nat.Static(*[nat.ptr(a) for a in self._static])
+        cws = None if cw_south is None else _f64(cw_south)
+        st = nat.Static(*[nat.ptr(a) for a in self._static],
+                        nat.ptr(cws) if cws is not None else None)
         h = ctypes.c_void_p()
         rc = L.bsq_create(ctypes.byref(desc), ctypes.byref(st),
                           ctypes.c_void_p(self.workspace.data_ptr()), self.nbytes,
@@ -99,6 +101,44 @@ class DeviceStep:
 
     def commit(self):
         nat.check(nat.lib().bsq_commit(self._h), "commit")
+
+    # -- y-strip sharding: phased step and workspace views -----------------------
+    def phase(self, ph: int, params=None):
+        p = ctypes.byref(params) if params is not None else None
+        rc = nat.lib().bsq_phase(self._h, ph, p, ctypes.byref(self._res))
+        if rc not in (nat.BSQ_OK, nat.BSQ_ERR_SINGULAR):
+            nat.check(rc, f"bsq_phase({ph})")
+        return rc, self._res
+
+    def factor_tail(self) -> np.ndarray:
+        out = np.empty(self.nx)
+        nat.check(nat.lib().bsq_factor_tail(self._h, nat.ptr(out)), "factor_tail")
+        return out
+
+    def pivot_flags(self):
+        pos, sing = ctypes.c_int(), ctypes.c_int()
+        nat.check(nat.lib().bsq_pivot_flags(self._h, ctypes.byref(pos), ctypes.byref(sing)),
+                  "pivot_flags")
+        return bool(pos.value), bool(sing.value)
+
+    def _layout(self, which: int):
+        off, pitch, xo, eb = ctypes.c_size_t(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        nat.check(nat.lib().bsq_array_layout(self._h, which, ctypes.byref(off), ctypes.byref(pitch),
+                                             ctypes.byref(xo), ctypes.byref(eb)), "array_layout")
+        return off.value, pitch.value, xo.value, eb.value
+
+    def rows(self, which: int) -> torch.Tensor:
+        """Torch view (ny+4, nx+4) of a padded device field inside the workspace."""
+        off, pitch, xo, eb = self._layout(which)
+        dt = torch.float64 if eb == 8 else torch.float32
+        n = (self.ny + 4) * pitch * eb
+        return self.workspace[off:off + n].view(dt).view(self.ny + 4, pitch)[:, xo:xo + self.nx + 4]
+
+    def vector(self, which: int) -> torch.Tensor:
+        """Torch view of an nx-long device vector (strip boundary values)."""
+        off, _, _, eb = self._layout(which)
+        dt = torch.float64 if eb == 8 else torch.float32
+        return self.workspace[off:off + self.nx * eb].view(dt)
 
     # -- kernel-level seams -------------------------------------------------
     def stage_rates(self):

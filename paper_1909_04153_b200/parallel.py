@@ -1,0 +1,462 @@
+"""y-strip sharding of the Boussinesq step across GPUs.
+
+Rank r owns interior rows [row0_r, row0_r + ny_r) of the global grid with
+the full x extent.  A step is the single-GPU step cut at its exchange
+points (include/bsq.h BSQ_PH_*):
+
+  GHOST     physical ghost strips            -> halo: 2 rows of w, P, Q
+  STAGE     fused stage + t+dt ghost strips
+  SOLVE1F   x lines (rank local) + y lines forward sweep, pipelined across
+            ranks: rank r continues each column's recurrence from rank r-1's
+            last dw (exactly the single-GPU Thomas operation sequence)
+  SOLVE1B   y lines back substitution, pipelined from the top rank down
+                                             -> halo: 1 row of P1, Q1
+  CORRECT   cross-correction right-hand sides
+  SOLVE2F/B second solve, as above
+  FINAL     finalize; reductions combined across ranks (max, NaN flag,
+            first bad cell as a global row-major index, clamped volume
+            summed in rank order)
+
+Every per-cell operation therefore sees the same operands as on one GPU, so
+a sharded run is bitwise identical to the single-GPU run (and so to the
+reference) -- checked by tests/test_gpu_sharded.py with the ranks emulated
+in one process on one GPU.
+
+Two transports: ``LocalComm`` keeps all strips in this process (device
+copies on one stream, sequential pipeline -- used for emulation/tests) and
+``DistComm`` holds one strip per process and moves halos and boundary
+vectors with torch.distributed (NCCL over NVLink on a multi-GPU box; its
+host-side logic is exercised with gloo on CPU by tests/test_parallel_host.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .device import DeviceStep
+from .grid import GHOST
+from .stepper import Simulator
+
+_N, _S = 0, 1  # side indices (bsq.h order N, S, E, W)
+_STATE = (nat.ARR_W, nat.ARR_P, nat.ARR_Q)
+_PENDING_PQ = (nat.ARR_P_NEW, nat.ARR_Q_NEW)
+
+
+def split_rows(ny: int, world: int) -> list[tuple[int, int]]:
+    """(row0, ny_r) per rank: as equal as possible, earlier ranks one larger."""
+    if world < 1 or ny < 5 * world:
+        raise ValueError(f"cannot split {ny} rows over {world} strips of >= 5 rows")
+    base, extra = divmod(ny, world)
+    out, r0 = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append((r0, n))
+        r0 += n
+    return out
+
+
+def strip_band(lo_g: int, len_g: int, row0: int, ny: int):
+    """Local part of a global N/S sponge band: (local lo, length, offset
+    into the global factor array)."""
+    lo = max(lo_g - row0, 0)
+    hi = min(lo_g + len_g - row0, ny)
+    if hi <= lo:
+        return 0, 0, 0
+    return lo, hi - lo, row0 + lo - lo_g
+
+
+class _StripStatic:
+    """The static fields of one strip: rows of the global padded arrays."""
+
+    def __init__(self, bathy, row0: int, ny: int):
+        rows = slice(row0, row0 + ny + 2 * GHOST)
+        self.bed_eff = bathy.bed_eff[rows]
+        self.depth = bathy.depth[rows]
+        self.depth_dx = bathy.depth_dx[rows]
+        self.depth_dy = bathy.depth_dy[rows]
+        self.bed_face_x = bathy.bed_face_x[rows]
+        self.bed_face_y = bathy.bed_face_y[row0:row0 + ny + 2 * GHOST - 1]
+
+
+# ---------------------------------------------------------------------------
+# transports
+
+
+class LocalComm:
+    """All strips in this process (one GPU): exchanges are device copies on
+    one stream, the y-line pipeline runs the strips in rank order."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.local = list(range(world))
+
+    def is_local(self, r):
+        return True
+
+    # setup: cw tails travel rank -> rank + 1
+    def pass_tail(self, tails: dict, r: int, tail):
+        tails[r] = tail
+
+    def get_tail(self, tails: dict, r: int, nx: int):
+        return tails[r - 1]
+
+    def any_flag(self, flags: list) -> bool:
+        return any(flags)
+
+    def halo(self, strips, ids, nrows: int, stream):
+        with torch.cuda.stream(stream):
+            for r in range(self.world - 1):
+                lo, up = strips[r], strips[r + 1]
+                n = lo.ny
+                for a in ids:
+                    L, U = lo.rows(a), up.rows(a)
+                    U[GHOST - nrows:GHOST].copy_(L[n + GHOST - nrows:n + GHOST])
+                    L[n + GHOST:n + GHOST + nrows].copy_(U[GHOST:GHOST + nrows])
+
+    def pipeline(self, strips, ph_f: int, ph_b: int, stream):
+        with torch.cuda.stream(stream):
+            for r in range(self.world):
+                if r > 0:
+                    strips[r].vector(nat.ARR_DW_IN).copy_(strips[r - 1].vector(nat.ARR_DW_OUT))
+                strips[r].phase(ph_f)
+            for r in reversed(range(self.world)):
+                if r < self.world - 1:
+                    strips[r].vector(nat.ARR_X_IN).copy_(strips[r + 1].vector(nat.ARR_X_OUT))
+                strips[r].phase(ph_b)
+
+    def reduce(self, parts: list, nx: int, rows0: list):
+        return _combine(parts, nx, rows0)
+
+    def gather_state(self, locals_: dict, shape, ranges):
+        return _assemble(locals_, shape, ranges)
+
+
+class DistComm:
+    """One strip per process; halos, boundary vectors and reductions over
+    torch.distributed (NCCL on GPUs; gloo for the CPU tests of this logic)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.local = [self.rank]
+
+    def _dev(self):
+        return torch.device("cuda", torch.cuda.current_device()) \
+            if self.dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+
+    def is_local(self, r):
+        return r == self.rank
+
+    def pass_tail(self, tails: dict, r: int, tail):
+        if r + 1 < self.world:
+            self.dist.send(torch.from_numpy(np.ascontiguousarray(tail)).to(self._dev()), r + 1,
+                           group=self.group)
+
+    def get_tail(self, tails: dict, r: int, nx: int):
+        buf = torch.empty(nx, dtype=torch.float64, device=self._dev())
+        self.dist.recv(buf, r - 1, group=self.group)
+        return buf.cpu().numpy()
+
+    def any_flag(self, flags: list) -> bool:
+        t = torch.tensor([1 if any(flags) else 0], dtype=torch.int64, device=self._dev())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return bool(t.item())
+
+    def _exchange(self, send_up, send_dn, recv_up, recv_dn):
+        """Post the four transfers with the neighbours (None = no neighbour)."""
+        d, r, ops = self.dist, self.rank, []
+        if send_up is not None:
+            ops.append(d.P2POp(d.isend, send_up, r + 1, group=self.group))
+            ops.append(d.P2POp(d.irecv, recv_up, r + 1, group=self.group))
+        if send_dn is not None:
+            ops.append(d.P2POp(d.isend, send_dn, r - 1, group=self.group))
+            ops.append(d.P2POp(d.irecv, recv_dn, r - 1, group=self.group))
+        if ops:
+            for w in d.batch_isend_irecv(ops):
+                w.wait()
+
+    def halo(self, strips, ids, nrows: int, stream):
+        s = strips[self.rank]
+        n = s.ny
+        up, dn = self.rank + 1 < self.world, self.rank > 0
+        with torch.cuda.stream(stream):
+            views = [s.rows(a) for a in ids]
+            send_up = torch.cat([v[n + GHOST - nrows:n + GHOST] for v in views]) if up else None
+            send_dn = torch.cat([v[GHOST:GHOST + nrows] for v in views]) if dn else None
+            recv_up = torch.empty_like(send_up) if up else None
+            recv_dn = torch.empty_like(send_dn) if dn else None
+            self._exchange(send_up, send_dn, recv_up, recv_dn)
+            for k, v in enumerate(views):
+                if up:
+                    v[n + GHOST:n + GHOST + nrows].copy_(recv_up[k * nrows:(k + 1) * nrows])
+                if dn:
+                    v[GHOST - nrows:GHOST].copy_(recv_dn[k * nrows:(k + 1) * nrows])
+
+    def pipeline(self, strips, ph_f: int, ph_b: int, stream):
+        d, r, s = self.dist, self.rank, strips[self.rank]
+        with torch.cuda.stream(stream):
+            if r > 0:
+                d.recv(s.vector(nat.ARR_DW_IN), r - 1, group=self.group)
+            s.phase(ph_f)
+            if r + 1 < self.world:
+                d.send(s.vector(nat.ARR_DW_OUT), r + 1, group=self.group)
+                d.recv(s.vector(nat.ARR_X_IN), r + 1, group=self.group)
+            s.phase(ph_b)
+            if r > 0:
+                d.send(s.vector(nat.ARR_X_OUT), r - 1, group=self.group)
+
+    def reduce(self, parts: list, nx: int, rows0: list):
+        mine = _combine(parts, nx, rows0)
+        d, dev = self.dist, self._dev()
+        mx = torch.tensor([mine["max_rate"], mine["max_speed"], mine["max_depth"],
+                           -1.0 if math.isnan(mine["max_dev"]) else mine["max_dev"]],
+                          dtype=torch.float64, device=dev)
+        nan = torch.tensor([1 if math.isnan(mine["max_dev"]) else 0], dtype=torch.int64, device=dev)
+        big = np.iinfo(np.int64).max
+        bad = torch.tensor([b if b >= 0 else big for b in mine["stage_bad"] + mine["state_bad"]],
+                           dtype=torch.int64, device=dev)
+        cl = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(self.world)]
+        d.all_reduce(mx, op=d.ReduceOp.MAX, group=self.group)
+        d.all_reduce(nan, op=d.ReduceOp.MAX, group=self.group)
+        d.all_reduce(bad, op=d.ReduceOp.MIN, group=self.group)
+        d.all_gather(cl, torch.tensor([mine["clamped"]], dtype=torch.float64, device=dev),
+                     group=self.group)
+        m = mx.cpu().numpy()
+        bads = [int(b) if b != big else -1 for b in bad.cpu().numpy()]
+        clamped = 0.0
+        for c in cl:  # rank order: deterministic
+            clamped += float(c.item())
+        return {"max_rate": float(m[0]), "max_speed": float(m[1]), "max_depth": float(m[2]),
+                "max_dev": math.nan if nan.item() else float(m[3]), "clamped": clamped,
+                "stage_bad": bads[:5], "state_bad": bads[5:]}
+
+    def gather_state(self, locals_: dict, shape, ranges):
+        (w, p, q), = locals_.values()
+        dev = self._dev()
+        outs = []
+        for a in (w, p, q):
+            t = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+            n_max = max(n for _, n in ranges) + 2 * GHOST
+            buf = torch.zeros((n_max, a.shape[1]), dtype=t.dtype, device=dev)
+            buf[:t.shape[0]] = t
+            bufs = [torch.empty_like(buf) for _ in range(self.world)]
+            self.dist.all_gather(bufs, buf, group=self.group)
+            outs.append([b.cpu().numpy() for b in bufs])
+        per = {r: tuple(outs[k][r][:ranges[r][1] + 2 * GHOST] for k in range(3))
+               for r in range(self.world)}
+        return _assemble(per, shape, ranges)
+
+
+def _combine(parts: list, nx: int, rows0: list) -> dict:
+    """Cross-strip reduction of per-strip step results, in rank order."""
+    out = {"max_rate": 0.0, "max_speed": 0.0, "max_depth": 0.0, "max_dev": 0.0, "clamped": 0.0,
+           "stage_bad": [-1] * 5, "state_bad": [-1] * 3}
+    nan = False
+    for res, row0 in zip(parts, rows0):
+        out["max_rate"] = max(out["max_rate"], res.max_rate)
+        out["max_speed"] = max(out["max_speed"], res.max_speed)
+        out["max_depth"] = max(out["max_depth"], res.max_depth)
+        if math.isnan(res.max_dev):
+            nan = True
+        else:
+            out["max_dev"] = max(out["max_dev"], res.max_dev)
+        out["clamped"] += res.clamped
+        for key, src in (("stage_bad", res.stage_bad), ("state_bad", res.state_bad)):
+            for k, b in enumerate(src):
+                if b >= 0:
+                    g = b + row0 * nx  # global row-major interior index
+                    cur = out[key][k]
+                    out[key][k] = g if cur < 0 else min(cur, g)
+    if nan:
+        out["max_dev"] = math.nan
+    return out
+
+
+def _assemble(per: dict, shape, ranges):
+    """Global padded arrays from per-strip padded arrays (interior rows of
+    every strip, ghost rows of the edge strips)."""
+    full = [np.empty(shape) for _ in range(3)]
+    last = len(ranges) - 1
+    for r, (row0, n) in enumerate(ranges):
+        lo = 0 if r == 0 else GHOST
+        hi = n + 2 * GHOST if r == last else n + GHOST
+        for k in range(3):
+            full[k][row0 + lo:row0 + hi] = per[r][k][lo:hi]
+    return tuple(full)
+
+
+# ---------------------------------------------------------------------------
+
+
+class ShardedDevice:
+    """Drop-in for DeviceStep over y-strips (the Simulator drives it)."""
+
+    def __init__(self, sim: "ShardedSimulator", desc, bathy, device, world: int, comm):
+        self.sim, self.comm, self.world = sim, comm, world
+        self.nx, self.ny = desc.nx, desc.ny
+        self.shape = (desc.ny + 2 * GHOST, desc.nx + 2 * GHOST)
+        self.ranges = split_rows(desc.ny, world)
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.stream = torch.cuda.Stream(dev)
+        self.strips: dict[int, DeviceStep] = {}
+        self._bands = []  # per rank: [(lo, len, off)] for N, S
+        tails: dict = {}
+        sing = []
+        for r, (row0, n) in enumerate(self.ranges):
+            bands = []
+            for s in (_N, _S):
+                bands.append(strip_band(desc.sponge_lo[s], desc.sponge_len[s], row0, n)
+                             if desc.sponge_len[s] else (0, 0, 0))
+            self._bands.append(bands)
+            if not comm.is_local(r):
+                continue
+            d = nat.Desc.from_buffer_copy(desc)
+            d.ny, d.row0, d.ny_global = n, row0, desc.ny
+            d.south_internal = 1 if r > 0 else 0
+            d.north_internal = 1 if r < world - 1 else 0
+            for s, (lo, ln, _) in zip((_N, _S), bands):
+                d.sponge_lo[s], d.sponge_len[s] = lo, ln
+            cws = comm.get_tail(tails, r, desc.nx) if r > 0 else None
+            strip = DeviceStep(d, _StripStatic(bathy, row0, n), device=dev, stream=self.stream,
+                               cw_south=cws)
+            self.strips[r] = strip
+            comm.pass_tail(tails, r, strip.factor_tail())
+            sing.append(strip.pivot_flags()[1])
+        self.singular = comm.any_flag(sing)
+        first = self.strips[min(self.strips)]
+        self.workspace = first.workspace
+        self._res = nat.StepResult()
+
+    # -- state -----------------------------------------------------------------------
+    def upload(self, w, p, q):
+        for r, s in self.strips.items():
+            row0, n = self.ranges[r]
+            rows = slice(row0, row0 + n + 2 * GHOST)
+            s.upload(w[rows], p[rows], q[rows])
+
+    def download(self, pending: bool = False, out=None):
+        per = {r: s.download(pending=pending) for r, s in self.strips.items()}
+        full = self.comm.gather_state(per, self.shape, self.ranges)
+        if out is not None:
+            for dst, src in zip(out, full):
+                dst[...] = src
+            return out
+        return full
+
+    def history(self, level: int, field: int) -> np.ndarray:
+        out = np.empty((self.ny, self.nx))
+        for r, s in self.strips.items():
+            row0, n = self.ranges[r]
+            out[row0:row0 + n] = s.history(level, field)
+        return out
+
+    def speed_extrema(self):
+        vals = [s.speed_extrema() for s in self.strips.values()]
+        res = [nat.StepResult() for _ in vals]
+        for rs, v in zip(res, vals):
+            rs.max_rate, rs.max_speed, rs.max_depth = v
+            rs.max_dev = 0.0
+            for k in range(5):
+                rs.stage_bad[k] = -1
+            for k in range(3):
+                rs.state_bad[k] = -1
+        m = self.comm.reduce(res, self.nx, [self.ranges[r][0] for r in self.strips])
+        return m["max_rate"], m["max_speed"], m["max_depth"]
+
+    # -- the sharded step ----------------------------------------------------------------
+    def _strip_params(self, params, r):
+        """params with this strip's part of the N/S sponge factors."""
+        p = nat.StepParams.from_buffer_copy(params)
+        for s, (lo, ln, off) in zip((_N, _S), self._bands[r]):
+            fac = self.sim._fac_keep[s]
+            p.sponge_fac[s] = nat.ptr(fac[off:]) if (ln and fac is not None) else None
+        return p
+
+    def step(self, params):
+        order = sorted(self.strips)
+        strips = self.strips
+        sp = {r: self._strip_params(params, r) for r in order}
+        for r in order:
+            strips[r].phase(nat.PH_GHOST, sp[r])
+        self.comm.halo(strips, _STATE, 2, self.stream)
+        for r in order:
+            strips[r].phase(nat.PH_STAGE)
+        self.comm.pipeline(strips, nat.PH_SOLVE1F, nat.PH_SOLVE1B, self.stream)
+        self.comm.halo(strips, _PENDING_PQ, 1, self.stream)
+        for r in order:
+            strips[r].phase(nat.PH_CORRECT)
+        self.comm.pipeline(strips, nat.PH_SOLVE2F, nat.PH_SOLVE2B, self.stream)
+        parts = []
+        for r in order:
+            _, res = strips[r].phase(nat.PH_FINAL)
+            parts.append(nat.StepResult.from_buffer_copy(res))
+        m = self.comm.reduce(parts, self.nx, [self.ranges[r][0] for r in order])
+        out = self._res
+        out.max_rate, out.max_speed, out.max_depth = m["max_rate"], m["max_speed"], m["max_depth"]
+        out.max_dev, out.clamped = m["max_dev"], m["clamped"]
+        for k in range(5):
+            out.stage_bad[k] = m["stage_bad"][k]
+        for k in range(3):
+            out.state_bad[k] = m["state_bad"][k]
+        rc = nat.BSQ_ERR_SINGULAR if self.singular else nat.BSQ_OK
+        return rc, out
+
+    def commit(self):
+        for s in self.strips.values():
+            s.commit()
+
+    def close(self):
+        for s in self.strips.values():
+            s.close()
+
+    # timing / introspection: the first local strip stands for the rank
+    def set_timing(self, on: bool):
+        for s in self.strips.values():
+            s.set_timing(on)
+
+    def kernel_times(self):
+        return self.strips[min(self.strips)].kernel_times()
+
+    def kernels_per_step(self) -> int:
+        return sum(s.kernels_per_step() + 2 for s in self.strips.values())
+
+    def stage_rates(self):
+        raise NotImplementedError("kernel-level seams are single-grid only")
+
+    solve_momentum = fill_ghosts = stage_rates
+
+
+class ShardedSimulator(Simulator):
+    """Simulator whose grid is split into y-strips, one per rank.
+
+    ``world`` strips emulated in this process when ``comm`` is None (one GPU,
+    bitwise-checkable against the single-GPU run), or ``comm=DistComm()``
+    under torchrun with one strip per process.  Inputs are the global
+    objects; every API is the Simulator's.
+    """
+
+    def __init__(self, *args, world: int | None = None, comm=None, **kw):
+        if comm is None:
+            comm = LocalComm(world or 1)
+        self._comm = comm
+        self._world = comm.world
+        super().__init__(*args, **kw)
+
+    def _make_device(self, desc, bathy, device):
+        if self.solver != "thomas":
+            raise NotImplementedError("sharded solves use the Thomas pipeline")
+        return ShardedDevice(self, desc, bathy, device, self._world, self._comm)
+
+    @property
+    def stream(self):
+        return self._dev.stream

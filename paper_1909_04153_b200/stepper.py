@@ -220,7 +220,8 @@ class Simulator:
         ph = self.phys
         d.g, d.b_disp, d.bp13, d.c_f = ph.g, ph.b_disp, ph.b_disp + 1.0 / 3.0, ph.c_f
         d.theta, d.h_eps, d.h_dry, d.ws = self.numerics.theta, bathy.h_eps, self.h_dry, bathy.ws
-        self._dev = DeviceStep(d, bathy, device=device)
+        self._fac_keep: list = [None] * 4
+        self._dev = self._make_device(d, bathy, device)
         self._dev.upload(state.w, state.p, state.q)
         self._host_state = None      # FieldState handed out by .state
         self._host_pristine = None   # what the device held when it was handed out
@@ -238,7 +239,10 @@ class Simulator:
         self._chain = controller.dt_init
         self._extrema = self._dev.speed_extrema()
         self._params = nat.StepParams()
-        self._fac_keep: list = [None] * 4
+
+    def _make_device(self, desc, bathy, device):
+        """The device engine for the whole grid (ShardedSimulator overrides)."""
+        return DeviceStep(desc, bathy, device=device)
 
     # -- implicit operator (host copy, for inspection and the warning) ----------
     def _warn_dominance(self):
