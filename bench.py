@@ -1,28 +1,31 @@
 """Benchmark: adaptive-AB3 Boussinesq steps on B200, Gcell-updates/s.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1)
 
 Workload (BASELINE.json configs[4]): rip-current barred
 beach with a 68-component JONSWAP wavemaker, walls, quadratic friction,
-4096 x 4096 cells per GPU, fp64, real adaptive steps (Euler bootstrap then
-variable-step AB3 with cross-correction), synthetic bathymetry built by the
-reference's own generator restated (paper Eq. 48).  Every field is 134 MB,
-larger than the 126 MB L2, so no L2 flush is needed between steps.
+4096 x 4096 cells per GPU (global 4096 x 4096N, y-strips, one per rank),
+fp64, real adaptive steps (Euler bootstrap then variable-step AB3 with
+cross-correction), synthetic bathymetry built by the reference's own
+generator restated (paper Eq. 48).  Every field is 134 MB, larger than the
+126 MB L2, so no L2 flush is needed between steps.
 
-Prints ONE JSON line (rank 0).  ``value``: cells x steps / device time with
-the state resident in HBM (CUDA events on the library stream, max over
+Prints ONE JSON line (rank 0).  ``value``: all cells x steps / device time
+with the state resident in HBM (CUDA events on the library stream, max over
 ranks).  ``e2e``: the same through the public ``Simulator`` API starting from
-host (pinned) buffers: initial state upload, K advance() calls (each: H2D
-step scalars, D2H reductions) and the final state download, all timed.
-``roofline``: the dominant kernel's algorithmic bytes / its event-timed
-duration vs the measured HBM copy bandwidth.  ``cpu_baseline``: the CPU
-oracle (C port of the reference step) on a bounded sample of the same
+host (pinned) buffers: state upload, K advance() calls (each: H2D step
+scalars, D2H reductions) and the state download, all timed.  ``roofline``:
+the dominant kernel's algorithmic bytes / its event-timed duration vs the
+measured HBM copy bandwidth.  ``cpu_baseline``: the CPU oracle (C port of the
+reference step, bitwise equal to it) on a bounded sample of the same
 workload.  ``--impl reference`` times that CPU implementation alone.
 """
 
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -44,7 +47,6 @@ KERNEL_BYTES = {
     "correct": 8 * 11,  # R base_u, base_v, F*_n, G*_n, P1, Q1, depth, d_x, d_y; W 2 RHS
     "solve2": 8 * 12,
     "final": 8 * 7,     # R w*, bed_eff, P2, Q2; W w, P, Q
-    "ghost_t": 0, "ghost_n": 0,
 }
 
 
@@ -58,7 +60,8 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+    """nvidia-smi clocks and throttle reasons; started before the warm-up so
+    the sampler is live through the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -67,6 +70,7 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.rows = []
+        self.mark = None
         self.proc = None
         self.thread = None
 
@@ -74,7 +78,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -86,9 +90,17 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append((time.perf_counter(), parts))
 
-    def stop(self):
+    def window(self, t0, t1):
+        """Samples taken in [t0, t1]; at least the 3 nearest if none fell inside."""
+        inside = [p for t, p in self.rows if t0 <= t <= t1]
+        if len(inside) < 3 and self.rows:
+            mid = 0.5 * (t0 + t1)
+            inside = [p for _, p in sorted(self.rows, key=lambda r: abs(r[0] - mid))[:3]]
+        return inside
+
+    def stop(self, t0, t1):
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -97,16 +109,21 @@ class ClockSampler:
                 self.proc.kill()
         if self.thread is not None:
             self.thread.join(timeout=5)
-        if not self.rows:
+        rows = self.window(t0, t1)
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[0]) for r in rows) if v is not None]
+        mx = [v for v in (num(r[1]) for r in rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4)
-                          if r[2 + k].lower() == "active"})
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[2 + k].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
 def dist_env():
@@ -118,7 +135,7 @@ def dist_env():
 
 def cpu_baseline(case, steps: int, threads: int):
     """Time the CPU oracle (C restatement of the reference step) on the
-    same case; returns Mcell-updates/s and the sample description."""
+    same case; returns Gcell-updates/s and the wall time."""
     from oracle import oracle as orc
     sim = orc.OracleSimulator(case.bathy, case.state.copy(), case.boundaries,
                               orc.OController(dt_init=case.dt_init), phys=case.phys,
@@ -132,10 +149,24 @@ def cpu_baseline(case, steps: int, threads: int):
     return cells * steps / dt / 1e9, dt
 
 
-def run_reference(args, case, rank):
+def config_dict(args, case, world):
+    g = case.bathy.grid
+    return {"workload": f"C5 rip channel + JONSWAP maker, 4096x4096 per GPU, global "
+                        f"{g.nx}x{g.ny}" + (", y-strips" if world > 1 else ""),
+            "nx": g.nx, "ny_per_gpu": g.ny // world, "ny_global": g.ny, "gpus": world,
+            "precision": "fp64", "solver": "thomas", "cross_correction": True,
+            "adaptive": True, "parallelism": f"y-strip x{world}" if world > 1 else "single",
+            "l2": "inputs larger than L2 (134 MB per field)"}
+
+
+def run_reference(args, rank):
+    """CPU reference arm: the oracle (bitwise = reference) on all host cores,
+    on the per-GPU workload (rank 0 only)."""
     if rank != 0:
         return
     from oracle import oracle as orc
+    from paper_1909_04153_b200.scenario import make_case
+    case = make_case("C4", scale=args.scale)
     threads = os.cpu_count() or 1
     sim = orc.OracleSimulator(case.bathy, case.state.copy(), case.boundaries,
                               orc.OController(dt_init=case.dt_init), phys=case.phys,
@@ -148,28 +179,20 @@ def run_reference(args, case, rank):
     wall = time.perf_counter() - t0
     cells = case.bathy.grid.nx * case.bathy.grid.ny
     v = cells * args.steps / wall / 1e9
+    cfg = config_dict(args, case, 1)
+    cfg["gpus"] = args.gpus
     line = {
         "impl": "reference", "metric": "Gcell-updates/s", "value": v, "unit": "Gcell-updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args, case),
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": v, "unit": "Gcell-updates/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full steps of {config_dict(args, case)['workload']}"
-                                   " on the C oracle (OpenMP, bitwise = reference)"},
+                         "sample": f"{args.steps} full 4096x4096 steps of the per-GPU workload on "
+                                   "the C oracle (OpenMP; bitwise = reference)"},
         "e2e": {"value": v, "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-
-
-def config_dict(args, case):
-    g = case.bathy.grid
-    return {"workload": f"C5 rip channel + JONSWAP maker, {g.nx}x{g.ny} per GPU" if args.gpus == 1
-            else f"C5 rip channel, {g.nx}x{g.ny} per GPU x {args.gpus}",
-            "nx": g.nx, "ny": g.ny, "gpus": args.gpus, "precision": "fp64",
-            "solver": "thomas", "cross_correction": True, "adaptive": True,
-            "l2": "inputs larger than L2 (134 MB per field)"}
 
 
 def main():
@@ -184,40 +207,62 @@ def main():
     args = ap.parse_args()
     rank, world, local = dist_env()
 
-    from paper_1909_04153_b200.scenario import make_case
-    case = make_case("C4", scale=args.scale)
-
     if args.impl == "reference":
-        run_reference(args, case, rank)
+        run_reference(args, rank)
         return
 
     import torch
+    from paper_1909_04153_b200 import _native as nat
     from paper_1909_04153_b200 import stepper
+    from paper_1909_04153_b200.grid import FieldState
+    from paper_1909_04153_b200.scenario import make_case
 
-    dist = None
+    dist = comm = None
     if world > 1:
         import torch.distributed as dist_mod
+        from paper_1909_04153_b200.parallel import DistComm, ShardedSimulator
         dist = dist_mod
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = DistComm()
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
-    cells = case.bathy.grid.nx * case.bathy.grid.ny
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+
+    case = make_case("C5", gpus=world, scale=args.scale)
+    cells_total = case.bathy.grid.nx * case.bathy.grid.ny
+    cells_gpu = cells_total // world
+
+    def make_sim(precision="fp64", state=None):
+        st = state if state is not None else case.state.copy()
+        kw = dict(phys=case.phys, device=dev, precision=precision)
+        ctrl = stepper.TimeController(dt_init=case.dt_init)
+        if world > 1:
+            return ShardedSimulator(case.bathy, st, case.boundaries, ctrl, comm=comm, **kw)
+        return stepper.Simulator(case.bathy, st, case.boundaries, ctrl, **kw)
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
 
     # ---- device-resident timing: value + per-kernel roofline ------------------
-    sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
-                            stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
-                            device=dev)
+    sim = make_sim()
     for _ in range(max(args.warmup, 3)):
         sim.advance()
     stream = sim._dev.stream
     sim._dev.set_timing(True)
     per_kernel = {}
-    clocks = ClockSampler(dev.index)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    clocks.start()
+    barrier()
+    t_c0 = time.perf_counter()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)
     for _ in range(args.steps):
@@ -226,53 +271,40 @@ def main():
             per_kernel.setdefault(name, []).append(ms)
     end.record(stream)
     torch.cuda.synchronize(dev)
-    clock_info = clocks.stop()
-    ms_total = start.elapsed_time(end)
-    if dist is not None:
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
-        dist.barrier()
+    t_c1 = time.perf_counter()
+    ms_total = max_over_ranks(start.elapsed_time(end))
     sim._dev.set_timing(False)
     ms_step = ms_total / args.steps
-    value = cells * world * args.steps / (ms_total * 1e-3) / 1e9
+    value = cells_total * args.steps / (ms_total * 1e-3) / 1e9
     kps = sim._dev.kernels_per_step()
     sim.close()
     del sim
     torch.cuda.empty_cache()
 
     # ---- the fp32 mode on the same workload (extra field; the headline is fp64) ----
-    sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
-                            stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
-                            device=dev, precision="fp32")
+    sim = make_sim("fp32")
     for _ in range(max(args.warmup, 3)):
         sim.advance()
-    torch.cuda.synchronize(dev)
+    barrier()
     s32, e32 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s32.record(sim._dev.stream)
     for _ in range(args.steps):
         sim.advance()
     e32.record(sim._dev.stream)
     torch.cuda.synchronize(dev)
-    ms32 = s32.elapsed_time(e32)
-    if dist is not None:
-        t = torch.tensor([ms32], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms32 = float(t.item())
-    v32 = cells * world * args.steps / (ms32 * 1e-3) / 1e9
-    hbm_, _ = peaks()
+    ms32 = max_over_ranks(s32.elapsed_time(e32))
+    v32 = cells_total * args.steps / (ms32 * 1e-3) / 1e9
+    hbm, peak_kind = peaks()
     fp32 = {"value": v32, "unit": "Gcell-updates/s", "ms_per_step": ms32 / args.steps,
-            "step_frac": v32 / world * (B_ALG_STEP // 2) / hbm_,
+            "step_frac": v32 / world * (B_ALG_STEP // 2) / hbm,
             "parity": "eta rel-L2 <= 1e-4, wet/dry mask exact (tests/test_gpu_fp32.py)"}
     sim.close()
     del sim
     torch.cuda.empty_cache()
 
-    hbm, peak_kind = peaks()
     avg = {k: float(np.mean(v)) for k, v in per_kernel.items()}
-    dom = max((k for k in avg if k in KERNEL_BYTES and KERNEL_BYTES[k] > 0), key=lambda k: avg[k])
-    bytes_launch = KERNEL_BYTES[dom] * cells
-    achieved = bytes_launch / (avg[dom] * 1e-3) / 1e9
+    dom = max((k for k in avg if k in KERNEL_BYTES), key=lambda k: avg[k])
+    achieved = KERNEL_BYTES[dom] * cells_gpu / (avg[dom] * 1e-3) / 1e9
     step_gbs = value / world * B_ALG_STEP
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
@@ -280,40 +312,30 @@ def main():
                 "step_bytes_per_cell": B_ALG_STEP}
 
     # ---- e2e through the public API from pinned host buffers --------------------
-    import torch as _t
-    pin = [_t.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
            for a in (case.state.w, case.state.p, case.state.q)]
-    pin_out = [_t.empty(a.shape, dtype=_t.float64).pin_memory().numpy() for a in pin]
-    from paper_1909_04153_b200.grid import FieldState
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
+    sim = make_sim(state=FieldState(*pin))
+    pin_out = [torch.empty(a.shape, dtype=torch.float64).pin_memory().numpy() for a in pin]
+    barrier()
     t0 = time.perf_counter()
-    sim = stepper.Simulator(case.bathy, FieldState(*pin), case.boundaries,
-                            stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
-                            device=dev)
-    t_setup = time.perf_counter()
-    sim.state = FieldState(*pin)  # the upload proper
+    sim.state = FieldState(*pin)  # upload (a rank uploads its strip)
     for _ in range(args.steps):
         sim.advance()
-    final = sim.download_state(out=pin_out)
-    t1 = time.perf_counter()
-    e2e_s = t1 - t_setup
-    if dist is not None:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    state_bytes = 3 * final.w.nbytes
-    import ctypes
-    from paper_1909_04153_b200 import _native as nat
+    if world > 1:
+        sim._dev.download_local(out=pin_out)  # each rank brings back its own strip
+    else:
+        sim.download_state(out=pin_out)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    state_bytes = 3 * 8 * (cells_gpu + 4 * case.bathy.grid.nx)
     h2d = state_bytes / args.steps + ctypes.sizeof(nat.StepParams)
     d2h = state_bytes / args.steps + ctypes.sizeof(nat.StepResult)
-    e2e = {"value": cells * world * args.steps / e2e_s / 1e9, "unit": "Gcell-updates/s",
+    e2e = {"value": cells_total * args.steps / e2e_s / 1e9, "unit": "Gcell-updates/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
            "includes": "state upload from pinned host + K advance() (H2D scalars, D2H "
                        "reductions) + final state download; excludes one-time setup "
-                       f"({t_setup - t0:.2f} s: static upload + LU factorization)"}
+                       "(static upload + LU factorization)"}
     sim.close()
+    clock_info = clocks.stop(t_c0, t_c1)
 
     # ---- CPU baseline (rank 0, N = 1 only) ------------------------------------------
     cpu = None
@@ -330,7 +352,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (rip-channel bathymetry, JONSWAP maker; reference generators)",
-            "config": config_dict(args, case), "roofline": roofline, "cpu_baseline": cpu,
+            "config": config_dict(args, case, world), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": kps * args.steps, "clocks": clock_info, "fp32": fp32,
         }
         print(json.dumps(line), flush=True)

@@ -353,6 +353,16 @@ class ShardedDevice:
             return out
         return full
 
+    def download_local(self, out):
+        """Copy only this process's strips into the matching rows of the
+        global arrays ``out`` (w, p, q): the distributed-I/O path."""
+        for r, s in self.strips.items():
+            row0, n = self.ranges[r]
+            rows = slice(row0, row0 + n + 2 * GHOST)
+            w, p, q = s.download()
+            out[0][rows], out[1][rows], out[2][rows] = w, p, q
+        return out
+
     def history(self, level: int, field: int) -> np.ndarray:
         out = np.empty((self.ny, self.nx))
         for r, s in self.strips.items():
