@@ -10,15 +10,22 @@
 //   compute_ustar_vstar (dispersion.py:120-149)
 //   Euler / AB3 predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
 // and writes the new stage level, the predicted w, U*, V* and the
-// quadrature bases.  Faces and fluxes live only in shared memory.
+// quadrature bases.  Faces and fluxes never leave registers.
 //
-// CTA = 32 x 8 cells.  Phases (each ends in __syncthreads):
-//   A  load w, P, Q (+ eta) for the tile and a 2-cell halo, and face beds
-//   B  faces of every cell once: x faces for columns -1..32, y faces for
-//      rows -1..8 of the tile (the reference evaluates each face once too)
-//   C  fluxes of the 33 x 8 x-interfaces and 32 x 9 y-interfaces, held in
-//      registers across a barrier and stored over the dead face buffers
-//   D  per-cell rates, dispersive terms, cross groups, U*/V*, predictor
+// Column walk.  A CTA covers 32 columns x (NW*R) rows; w, P, Q and eta of the
+// tile plus a 2-cell halo are staged in shared memory once (the only
+// barrier).  Lane l of warp k owns column I0+l and walks rows
+// J0+k*R .. J0+k*R+R-1 upwards:
+//   y direction: the faces of row J+1 and the flux through the J|J+1 face
+//     are computed once and carried to the next row, where they are the
+//     south face/flux -- every y interface is evaluated exactly once;
+//   x direction: each lane evaluates its own cell's faces and the flux
+//     through its west face; the west neighbour's east face and the east
+//     neighbour's west flux arrive by warp shuffle.  The tile's edge cells
+//     (column I0-1's east face, and the flux through the tile's east edge)
+//     are batched for all R rows in one pre-pass on R lanes.
+// Every interface flux is a function of the same face values as in the
+// reference, so the result is bitwise the reference's.
 #include <cmath>
 #include <cstdint>
 
@@ -27,84 +34,39 @@
 
 namespace bsq {
 
-constexpr int TX = 32, TY = 8, NT = TX * TY;
-constexpr int HX = TX + 4, HY = TY + 4;       // tile + 2-cell halo
-constexpr int FXW = TX + 2, FYH = TY + 2;     // cells with x faces per row / rows with y faces
-constexpr int NXF = TY * FXW, NYF = FYH * TX; // face items
-constexpr int NXI = TY * (TX + 1), NYI = (TY + 1) * TX;  // interface items
-constexpr int NFL = NXI + NYI;
-constexpr int FL_PASSES = (NFL + NT - 1) / NT;
+constexpr int SW_ = 32;          // columns per CTA (one per lane)
+constexpr int SNW = 4;           // warps per CTA
+constexpr int SR = 8;            // rows per warp
+constexpr int STY = SNW * SR;    // rows per CTA
+constexpr int SHX = SW_ + 4, SHY = STY + 4;
+constexpr unsigned FULL = 0xffffffffu;
+static_assert(SR <= 16, "edge pre-pass uses lanes 0..SR-1 and 16..16+SR-1");
 
 template <class T>
 struct StageSmem {
-    T w[HY][HX], p[HY][HX], q[HY][HX], eta[HY][HX];
-    T bfx[TY][TX + 3];  // bed_face_x for columns -2..TX
-    T bfy[TY + 3][TX];  // bed_face_y for rows -2..TY
-    union {
-        struct {  // phase B/C: faces (hi = east/north, lo = west/south)
-            T xwhi[TY][FXW], xwlo[TY][FXW], xphi[TY][FXW], xplo[TY][FXW], xqhi[TY][FXW],
-                xqlo[TY][FXW];
-            T ywhi[FYH][TX], ywlo[FYH][TX], yphi[FYH][TX], yplo[FYH][TX], yqhi[FYH][TX],
-                yqlo[FYH][TX];
-        } f;
-        struct {  // phase C/D: fluxes through the tile's interfaces
-            T fx[3][TY][TX + 1];
-            T fy[3][TY + 1][TX];
-        } x;
-    } u;
+    T w[SHY][SHX], p[SHY][SHX], q[SHY][SHX], eta[SHY][SHX];
 };
 
-// cu_flux (bsq_device.cuh) with the two divisions by each side's depth
-// sharing one correctly rounded reciprocal: ul = nl/dl and nl*tl/dl are
-// still the correctly rounded quotients.
 template <class T>
-__device__ __forceinline__ void cu_flux_rcp(T wl, T wr, T nl_, T nr_, T tl_, T tr_, T bf, T g,
-                                            T h_eps, T &f_mass, T &f_norm, T &f_tang) {
-    T hl = wl - bf;
-    if (hl < T(0)) hl = T(0);
-    T hr = wr - bf;
-    if (hr < T(0)) hr = T(0);
-    const T nl = hl > T(0) ? nl_ : T(0), tl = hl > T(0) ? tl_ : T(0);
-    const T nr = hr > T(0) ? nr_ : T(0), tr = hr > T(0) ? tr_ : T(0);
-    const T dl = hl > h_eps ? hl : h_eps;
-    const T dr = hr > h_eps ? hr : h_eps;
-    const T rl = rcp_rn(dl), rr = rcp_rn(dr);
-    const T ul = div_rcp(nl, dl, rl);
-    const T ur = div_rcp(nr, dr, rr);
-    const T cl = sqrt(g * hl);
-    const T cr = sqrt(g * hr);
-    const T ap = nb_max(nb_max(ul + cl, ur + cr), T(0));
-    const T am = nb_min(nb_min(ul - cl, ur - cr), T(0));
-    if (ap == T(0) && am == T(0)) {
-        f_mass = T(0);
-        f_norm = T(0);
-        f_tang = T(0);
-        return;
-    }
-    const T inv = rcp_rn(ap - am);
-    const T diff = ap * am * inv;
-    const T fnl = nl * ul + T(0.5) * g * hl * hl;
-    const T fnr = nr * ur + T(0.5) * g * hr * hr;
-    const T ftl = div_rcp(nl * tl, dl, rl);
-    const T ftr = div_rcp(nr * tr, dr, rr);
-    f_mass = (ap * nl - am * nr) * inv + diff * (wr - wl);
-    f_norm = (ap * fnl - am * fnr) * inv + diff * (nr - nl);
-    f_tang = (ap * ftl - am * ftr) * inv + diff * (tr - tl);
-}
+__device__ __forceinline__ T shfl_idx(T v, int src) { return __shfl_sync(FULL, v, src); }
+template <class T>
+__device__ __forceinline__ T shfl_up1(T v) { return __shfl_up_sync(FULL, v, 1); }
+template <class T>
+__device__ __forceinline__ T shfl_dn1(T v) { return __shfl_down_sync(FULL, v, 1); }
 
 template <class T>
-__global__ void __launch_bounds__(NT, 4) k_stage(Consts<T> C, const DevParams *__restrict__ P,
-                                                 StagePtrs<T> A, int predict) {
+__global__ void __launch_bounds__(SW_ *SNW) k_stage(Consts<T> C, const DevParams *__restrict__ P,
+                                                   StagePtrs<T> A, int predict) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StageSmem<T> &S = *reinterpret_cast<StageSmem<T> *>(smem_raw);
     const Layout L = C.L;
     const int nx = L.nx, ny = L.ny, nxt = nx + 4, nyt = ny + 4;
-    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
-    const int I0 = GL + blockIdx.x * TX, J0 = GL + blockIdx.y * TY;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int I0 = GL + blockIdx.x * SW_, J0 = GL + blockIdx.y * STY;
 
-    // ---- A: tile + halo ------------------------------------------------------
-    for (int k = tid; k < HY * HX; k += NT) {
-        const int y = k / HX, x = k - y * HX;
+    // ---- tile + 2-cell halo; eta = (w - bed_eff) - depth (dispersion.py:87) ----
+    for (int k = threadIdx.x; k < SHY * SHX; k += SW_ * SNW) {
+        const int y = k / SHX, x = k - y * SHX;
         const int J = J0 - 2 + y, I = I0 - 2 + x;
         T w = 0, p = 0, q = 0, e = 0;
         if (J < nyt && I < nxt) {
@@ -112,212 +74,216 @@ __global__ void __launch_bounds__(NT, 4) k_stage(Consts<T> C, const DevParams *_
             w = A.w[o];
             p = A.p[o];
             q = A.q[o];
-            e = (w - A.be[o]) - A.dep[o];  // dispersion.py:87
+            e = (w - A.be[o]) - A.dep[o];
         }
         S.w[y][x] = w;
         S.p[y][x] = p;
         S.q[y][x] = q;
         S.eta[y][x] = e;
     }
-    for (int k = tid; k < TY * (TX + 3); k += NT) {
-        const int y = k / (TX + 3), x = k - y * (TX + 3);
-        const int J = J0 + y, I = I0 - 2 + x;
-        S.bfx[y][x] = (J < nyt && I <= nx + 2) ? A.bfx[L.at(J, I)] : T(0);
-    }
-    for (int k = tid; k < (TY + 3) * TX; k += NT) {
-        const int y = k / TX, x = k - y * TX;
-        const int J = J0 - 2 + y, I = I0 + x;
-        S.bfy[y][x] = (J <= ny + 2 && I < nxt) ? A.bfy[L.at(J, I)] : T(0);
-    }
     __syncthreads();
 
-    // ---- B: faces, once per cell ------------------------------------------------
-    for (int k = tid; k < NXF + NYF; k += NT) {
-        if (k < NXF) {  // x faces of cell (row r, column c-1), c = 0..TX+1
-            const int r = k / FXW, c = k - r * FXW;
-            const int y = r + 2, x = c + 1;  // smem coords of the cell
-            const Faces<T> f = cell_faces(S.w[y][x - 1], S.w[y][x], S.w[y][x + 1], S.p[y][x - 1],
-                                          S.p[y][x], S.p[y][x + 1], S.q[y][x - 1], S.q[y][x],
-                                          S.q[y][x + 1], S.bfx[r][c + 1], S.bfx[r][c], C.theta);
-            S.u.f.xwhi[r][c] = f.whi;
-            S.u.f.xwlo[r][c] = f.wlo;
-            S.u.f.xphi[r][c] = f.phi;
-            S.u.f.xplo[r][c] = f.plo;
-            S.u.f.xqhi[r][c] = f.qhi;
-            S.u.f.xqlo[r][c] = f.qlo;
-        } else {  // y faces of cell (row r-1, column c), r = 0..TY+1
-            const int kk = k - NXF;
-            const int r = kk / TX, c = kk - r * TX;
-            const int y = r + 1, x = c + 2;
-            const Faces<T> f = cell_faces(S.w[y - 1][x], S.w[y][x], S.w[y + 1][x], S.p[y - 1][x],
-                                          S.p[y][x], S.p[y + 1][x], S.q[y - 1][x], S.q[y][x],
-                                          S.q[y + 1][x], S.bfy[r + 1][c], S.bfy[r][c], C.theta);
-            S.u.f.ywhi[r][c] = f.whi;
-            S.u.f.ywlo[r][c] = f.wlo;
-            S.u.f.yphi[r][c] = f.phi;
-            S.u.f.yplo[r][c] = f.plo;
-            S.u.f.yqhi[r][c] = f.qhi;
-            S.u.f.yqlo[r][c] = f.qlo;
+    const int I = I0 + lane, x = lane + 2;  // this lane's column (padded / smem)
+    const int jw = J0 + warp * SR;          // first row of this warp
+    const T g = C.g, h_eps = C.h_eps, theta = C.theta;
+    // bed on face (J, col) -- clamped to the array for out-of-grid lanes
+    auto bfx_at = [&](int J, int col) -> T {
+        return (J < nyt && col <= nx + 2) ? A.bfx[L.at(J, col)] : T(0);
+    };
+    auto bfy_at = [&](int J, int col) -> T {
+        return (J <= ny + 2 && col < nxt) ? A.bfy[L.at(J, col)] : T(0);
+    };
+    // x faces of the cell at smem (yy, xx), face beds bhi (east), blo (west)
+    auto xfaces = [&](int yy, int xx, T bhi, T blo) {
+        return cell_faces(S.w[yy][xx - 1], S.w[yy][xx], S.w[yy][xx + 1], S.p[yy][xx - 1],
+                          S.p[yy][xx], S.p[yy][xx + 1], S.q[yy][xx - 1], S.q[yy][xx],
+                          S.q[yy][xx + 1], bhi, blo, theta);
+    };
+    auto yfaces = [&](int yy, int xx, T bhi, T blo) {
+        return cell_faces(S.w[yy - 1][xx], S.w[yy][xx], S.w[yy + 1][xx], S.p[yy - 1][xx],
+                          S.p[yy][xx], S.p[yy + 1][xx], S.q[yy - 1][xx], S.q[yy][xx],
+                          S.q[yy + 1][xx], bhi, blo, theta);
+    };
+
+    // ---- x edge pre-pass (lanes 0..SR-1: one row each) --------------------------
+    // east face of column I0-1, and the flux through the tile's east edge
+    // (between columns I0+31 and I0+32), for rows jw .. jw+SR-1
+    T e_w = 0, e_p = 0, e_q = 0, fe1 = 0, fe2 = 0, fe3 = 0;
+    if (lane < SR) {
+        const int J = jw + lane, yy = J - (J0 - 2);
+        const Faces<T> fw = xfaces(yy, 1, bfx_at(J, I0 - 1), bfx_at(J, I0 - 2));
+        e_w = fw.whi;
+        e_p = fw.phi;
+        e_q = fw.qhi;
+        const T b31 = bfx_at(J, I0 + 31);
+        const Faces<T> fl = xfaces(yy, SW_ + 1, b31, bfx_at(J, I0 + 30));
+        const Faces<T> fr = xfaces(yy, SW_ + 2, bfx_at(J, I0 + 32), b31);
+        cu_flux_rcp(fl.whi, fr.wlo, fl.phi, fr.plo, fl.qhi, fr.qlo, b31, g, h_eps, fe1, fe2, fe3);
+    }
+
+    // ---- y pre-pass: faces of rows jw-1 and jw, flux through their face ---------
+    T bfy_s = bfy_at(jw - 1, I);  // bed on the south face of the current row
+    T bfy_n = bfy_at(jw, I);
+    Faces<T> yc;  // y faces of the current row (only the north face is used)
+    T fs1, fs2, fs3;
+    {
+        const int yy = jw - (J0 - 2);
+        const Faces<T> ys = yfaces(yy - 1, x, bfy_s, bfy_at(jw - 2, I));
+        yc = yfaces(yy, x, bfy_n, bfy_s);
+        T fq, fp;  // normal momentum is Q, tangential is P: fy2 = P flux, fy3 = Q flux
+        cu_flux_rcp(ys.whi, yc.wlo, ys.qhi, yc.qlo, ys.phi, yc.plo, bfy_s, g, h_eps, fs1, fq, fp);
+        fs2 = fp;
+        fs3 = fq;
+    }
+
+    T bfx_e = bfx_at(jw, I);  // prefetch row jw's face beds
+    for (int r = 0; r < SR; r++) {
+        const int J = jw + r, yy = J - (J0 - 2);
+        // -- x: own faces, the west flux, the east flux from the east lane --
+        const T bx_e = bfx_e;                       // bed_face_x[J][I]
+        T bx_w = shfl_up1(bx_e);                    // bed_face_x[J][I-1]
+        if (lane == 0) bx_w = bfx_at(J, I0 - 1);
+        if (r + 1 < SR) bfx_e = bfx_at(J + 1, I);
+        const Faces<T> xf = xfaces(yy, x, bx_e, bx_w);
+        T lw = shfl_up1(xf.whi), lp = shfl_up1(xf.phi), lq = shfl_up1(xf.qhi);
+        const T ew = shfl_idx(e_w, r), ep = shfl_idx(e_p, r), eq = shfl_idx(e_q, r);
+        if (lane == 0) {
+            lw = ew;
+            lp = ep;
+            lq = eq;
         }
-    }
-    __syncthreads();
-
-    // ---- C: fluxes (registers across the barrier, then over the faces) ----------
-    T fl[FL_PASSES][3];
-#pragma unroll
-    for (int s = 0; s < FL_PASSES; s++) {
-        const int k = tid + s * NT;
-        if (k < NXI) {  // interface between tile columns xi-1 and xi, row r
-            const int r = k / (TX + 1), xi = k - r * (TX + 1);
-            // left cell = face column xi, right cell = face column xi+1
-            cu_flux_rcp(S.u.f.xwhi[r][xi], S.u.f.xwlo[r][xi + 1], S.u.f.xphi[r][xi],
-                        S.u.f.xplo[r][xi + 1], S.u.f.xqhi[r][xi], S.u.f.xqlo[r][xi + 1],
-                        S.bfx[r][xi + 1], C.g, C.h_eps, fl[s][0], fl[s][1], fl[s][2]);
-        } else if (k < NFL) {  // interface between tile rows yi-1 and yi, column c
-            const int kk = k - NXI;
-            const int yi = kk / TX, c = kk - yi * TX;
-            // south cell = face row yi, north cell = face row yi+1; normal = Q
-            T f1, fq, fp;
-            cu_flux_rcp(S.u.f.ywhi[yi][c], S.u.f.ywlo[yi + 1][c], S.u.f.yqhi[yi][c],
-                        S.u.f.yqlo[yi + 1][c], S.u.f.yphi[yi][c], S.u.f.yplo[yi + 1][c],
-                        S.bfy[yi + 1][c], C.g, C.h_eps, f1, fq, fp);
-            fl[s][0] = f1;
-            fl[s][1] = fp;  // fy2 carries P
-            fl[s][2] = fq;  // fy3 carries Q
+        T fw1, fw2, fw3;  // flux through the west face of this cell
+        cu_flux_rcp(lw, xf.wlo, lp, xf.plo, lq, xf.qlo, bx_w, g, h_eps, fw1, fw2, fw3);
+        T fe_1 = shfl_dn1(fw1), fe_2 = shfl_dn1(fw2), fe_3 = shfl_dn1(fw3);
+        const T g1 = shfl_idx(fe1, r), g2 = shfl_idx(fe2, r), g3 = shfl_idx(fe3, r);
+        if (lane == SW_ - 1) {
+            fe_1 = g1;
+            fe_2 = g2;
+            fe_3 = g3;
         }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < FL_PASSES; s++) {
-        const int k = tid + s * NT;
-        if (k < NXI) {
-            const int r = k / (TX + 1), xi = k - r * (TX + 1);
-            S.u.x.fx[0][r][xi] = fl[s][0];
-            S.u.x.fx[1][r][xi] = fl[s][1];
-            S.u.x.fx[2][r][xi] = fl[s][2];
-        } else if (k < NFL) {
-            const int kk = k - NXI;
-            const int yi = kk / TX, c = kk - yi * TX;
-            S.u.x.fy[0][yi][c] = fl[s][0];
-            S.u.x.fy[1][yi][c] = fl[s][1];
-            S.u.x.fy[2][yi][c] = fl[s][2];
+        // -- y: faces of row J+1, flux through the J|J+1 face (carried north) --
+        const T bfy_nn = bfy_at(J + 1, I);
+        const Faces<T> yn = yfaces(yy + 1, x, bfy_nn, bfy_n);
+        T fn1, fnq, fnp;
+        cu_flux_rcp(yc.whi, yn.wlo, yc.qhi, yn.qlo, yc.phi, yn.plo, bfy_n, g, h_eps, fn1, fnq, fnp);
+        const T fn2 = fnp, fn3 = fnq;
+
+        if (J < ny + GL && I < nx + GL) {
+            const long o = L.at(J, I);
+            const T wc = S.w[yy][x], pc = S.p[yy][x], qc = S.q[yy][x];
+            // fv_rates (_kernels.py:230-251)
+            T rw = -(fe_1 - fw1) * C.inv_dx - (fn1 - fs1) * C.inv_dy;
+            const T src_x = -g * (wc - T(0.5) * (bx_e + bx_w)) * (bx_e - bx_w) * C.inv_dx;
+            const T src_y = -g * (wc - T(0.5) * (bfy_n + bfy_s)) * (bfy_n - bfy_s) * C.inv_dy;
+            T h = wc - A.be[o];
+            if (h < T(0)) h = T(0);
+            const T hstar = h > h_eps ? h : h_eps;
+            T fric = T(0);
+            if (C.c_f > T(0)) fric = C.c_f * sqrt(pc * pc + qc * qc) / (hstar * hstar);
+            T rp = -(fe_2 - fw2) * C.inv_dx - (fn2 - fs2) * C.inv_dy + src_x - fric * pc;
+            T rq = -(fe_3 - fw3) * C.inv_dx - (fn3 - fs3) * C.inv_dy + src_y - fric * qc;
+
+            const T d = A.dep[o], dx_ = A.ddx[o], dy_ = A.ddy[o];
+            T fs_ = T(0), gs_ = T(0);
+            if (d > T(0)) {
+                // dispersive_rates (_kernels.py:269-288)
+                const T(*E)[SHX] = S.eta;
+                const T ec = E[yy][x];
+                const T e_xx = (E[yy][x + 1] - T(2) * ec + E[yy][x - 1]) * C.inv_dx2;
+                const T e_yy = (E[yy + 1][x] - T(2) * ec + E[yy - 1][x]) * C.inv_dy2;
+                const T e_xy = (E[yy + 1][x + 1] - E[yy + 1][x - 1] - E[yy - 1][x + 1] +
+                                E[yy - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+                const T e_xxx = (E[yy][x + 2] - T(2) * E[yy][x + 1] + T(2) * E[yy][x - 1] -
+                                 E[yy][x - 2]) * T(0.5) * C.inv_dx * C.inv_dx2;
+                const T e_yyy = (E[yy + 2][x] - T(2) * E[yy + 1][x] + T(2) * E[yy - 1][x] -
+                                 E[yy - 2][x]) * T(0.5) * C.inv_dy * C.inv_dy2;
+                const T e_xyy = ((E[yy + 1][x + 1] - T(2) * E[yy][x + 1] + E[yy - 1][x + 1]) -
+                                 (E[yy + 1][x - 1] - T(2) * E[yy][x - 1] + E[yy - 1][x - 1])) *
+                                T(0.5) * C.inv_dx * C.inv_dy2;
+                const T e_xxy = ((E[yy + 1][x + 1] - T(2) * E[yy + 1][x] + E[yy + 1][x - 1]) -
+                                 (E[yy - 1][x + 1] - T(2) * E[yy - 1][x] + E[yy - 1][x - 1])) *
+                                T(0.5) * C.inv_dy * C.inv_dx2;
+                const T gd2 = g * d * d;
+                const T gd3 = gd2 * d;
+                rp += C.b_disp * gd3 * (e_xxx + e_xyy) +
+                      C.b_disp * gd2 * (dx_ * (T(2) * e_xx + e_yy) + dy_ * e_xy);
+                rq += C.b_disp * gd3 * (e_yyy + e_xxy) +
+                      C.b_disp * gd2 * (dy_ * (T(2) * e_yy + e_xx) + dx_ * e_xy);
+                // cross_rates (_kernels.py:310-321)
+                const T(*Q)[SHX] = S.q;
+                const T(*Pp)[SHX] = S.p;
+                const T q_x = (Q[yy][x + 1] - Q[yy][x - 1]) * T(0.5) * C.inv_dx;
+                const T q_y = (Q[yy + 1][x] - Q[yy - 1][x]) * T(0.5) * C.inv_dy;
+                const T q_xy = (Q[yy + 1][x + 1] - Q[yy + 1][x - 1] - Q[yy - 1][x + 1] +
+                                Q[yy - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+                const T p_x = (Pp[yy][x + 1] - Pp[yy][x - 1]) * T(0.5) * C.inv_dx;
+                const T p_y = (Pp[yy + 1][x] - Pp[yy - 1][x]) * T(0.5) * C.inv_dy;
+                const T p_xy = (Pp[yy + 1][x + 1] - Pp[yy + 1][x - 1] - Pp[yy - 1][x + 1] +
+                                Pp[yy - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+                const T sixth = div_static(d, C.six, C.r_six);
+                const T d2 = C.bp13 * d * d;
+                fs_ = sixth * (dx_ * q_y + dy_ * q_x) + d2 * q_xy;
+                gs_ = sixth * (dx_ * p_y + dy_ * p_x) + d2 * p_xy;
+            }
+
+            // non-finite stage values (dispersion.py:92-98): first row-major cell
+            const unsigned long long lin = (unsigned long long)(J - GL) * nx + (I - GL);
+            if (!isfinite(rw)) atomicMin(&A.bad[0], lin);
+            if (!isfinite(rp)) atomicMin(&A.bad[1], lin);
+            if (!isfinite(rq)) atomicMin(&A.bad[2], lin);
+            if (!isfinite(fs_)) atomicMin(&A.bad[3], lin);
+            if (!isfinite(gs_)) atomicMin(&A.bad[4], lin);
+            A.h0[0][o] = rw;
+            A.h0[1][o] = rp;
+            A.h0[2][o] = rq;
+            A.h0[3][o] = fs_;
+            A.h0[4][o] = gs_;
+
+            if (predict) {
+                // U*, V* (dispersion.py:131-148): divisions by grid constants
+                const T pe = S.p[yy][x + 1], pw = S.p[yy][x - 1];
+                const T qn = S.q[yy + 1][x], qs = S.q[yy - 1][x];
+                const T p_x = div_static(pe - pw, C.two_dx, C.r_two_dx);
+                const T p_xx = div_static(pe - T(2) * pc + pw, C.dx2, C.r_dx2);
+                const T ustar =
+                    pc - div_static(d * dx_, C.three, C.r_three) * p_x - C.bp13 * d * d * p_xx;
+                const T q_y = div_static(qn - qs, C.two_dy, C.r_two_dy);
+                const T q_yy = div_static(qn - T(2) * qc + qs, C.dy2, C.r_dy2);
+                const T vstar =
+                    qc - div_static(d * dy_, C.three, C.r_three) * q_y - C.bp13 * d * d * q_yy;
+                // predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
+                T wn, bu, bv, us, vs;
+                if (P->euler) {
+                    const T dt = T(P->dt);
+                    wn = wc + dt * rw;
+                    bu = ustar + dt * rp;
+                    bv = vstar + dt * rq;
+                    us = bu;
+                    vs = bv;
+                } else {
+                    const T wc0 = T(P->wc), wp1 = T(P->wp), wp2 = T(P->wp2);
+                    const T s0 = T(P->sc), s1 = T(P->sp), s2 = T(P->sp2);
+                    wn = wc + (wc0 * rw + wp1 * A.h1[0][o] + wp2 * A.h2[0][o]);
+                    bu = ustar + (wc0 * rp + wp1 * A.h1[1][o] + wp2 * A.h2[1][o]);
+                    bv = vstar + (wc0 * rq + wp1 * A.h1[2][o] + wp2 * A.h2[2][o]);
+                    us = bu + (s0 * fs_ + s1 * A.h1[3][o] + s2 * A.h2[3][o]);
+                    vs = bv + (s0 * gs_ + s1 * A.h1[4][o] + s2 * A.h2[4][o]);
+                }
+                A.wn[o] = wn;
+                A.bu[o] = bu;
+                A.bv[o] = bv;
+                A.us[o] = us;
+                A.vs[o] = vs;
+            }
         }
+        // carry north: this row's north face/flux is the next row's south
+        yc = yn;
+        fs1 = fn1;
+        fs2 = fn2;
+        fs3 = fn3;
+        bfy_s = bfy_n;
+        bfy_n = bfy_nn;
     }
-    __syncthreads();
-
-    // ---- D: per cell ----------------------------------------------------------------
-    const int J = J0 + ty, I = I0 + tx;
-    if (J >= ny + GL || I >= nx + GL) return;
-    const int y = ty + 2, x = tx + 2;
-    const long o = L.at(J, I);
-    const T wc = S.w[y][x], pc = S.p[y][x], qc = S.q[y][x];
-    const T be_ = S.bfx[ty][tx + 2], bw_ = S.bfx[ty][tx + 1];
-    const T bn_ = S.bfy[ty + 2][tx], bs_ = S.bfy[ty + 1][tx];
-
-    // fv_rates (_kernels.py:230-251)
-    T rw = -(S.u.x.fx[0][ty][tx + 1] - S.u.x.fx[0][ty][tx]) * C.inv_dx -
-           (S.u.x.fy[0][ty + 1][tx] - S.u.x.fy[0][ty][tx]) * C.inv_dy;
-    const T src_x = -C.g * (wc - T(0.5) * (be_ + bw_)) * (be_ - bw_) * C.inv_dx;
-    const T src_y = -C.g * (wc - T(0.5) * (bn_ + bs_)) * (bn_ - bs_) * C.inv_dy;
-    T h = wc - A.be[o];
-    if (h < T(0)) h = T(0);
-    const T hstar = h > C.h_eps ? h : C.h_eps;
-    T fric = T(0);
-    if (C.c_f > T(0)) fric = C.c_f * sqrt(pc * pc + qc * qc) / (hstar * hstar);
-    T rp = -(S.u.x.fx[1][ty][tx + 1] - S.u.x.fx[1][ty][tx]) * C.inv_dx -
-           (S.u.x.fy[1][ty + 1][tx] - S.u.x.fy[1][ty][tx]) * C.inv_dy + src_x - fric * pc;
-    T rq = -(S.u.x.fx[2][ty][tx + 1] - S.u.x.fx[2][ty][tx]) * C.inv_dx -
-           (S.u.x.fy[2][ty + 1][tx] - S.u.x.fy[2][ty][tx]) * C.inv_dy + src_y - fric * qc;
-
-    const T d = A.dep[o], dx_ = A.ddx[o], dy_ = A.ddy[o];
-    T fs_, gs_;
-    if (d > T(0)) {
-        // dispersive_rates (_kernels.py:269-288)
-        const T ec = S.eta[y][x];
-        const T e_xx = (S.eta[y][x + 1] - T(2) * ec + S.eta[y][x - 1]) * C.inv_dx2;
-        const T e_yy = (S.eta[y + 1][x] - T(2) * ec + S.eta[y - 1][x]) * C.inv_dy2;
-        const T e_xy = (S.eta[y + 1][x + 1] - S.eta[y + 1][x - 1] - S.eta[y - 1][x + 1] +
-                        S.eta[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
-        const T e_xxx = (S.eta[y][x + 2] - T(2) * S.eta[y][x + 1] + T(2) * S.eta[y][x - 1] -
-                         S.eta[y][x - 2]) * T(0.5) * C.inv_dx * C.inv_dx2;
-        const T e_yyy = (S.eta[y + 2][x] - T(2) * S.eta[y + 1][x] + T(2) * S.eta[y - 1][x] -
-                         S.eta[y - 2][x]) * T(0.5) * C.inv_dy * C.inv_dy2;
-        const T e_xyy = ((S.eta[y + 1][x + 1] - T(2) * S.eta[y][x + 1] + S.eta[y - 1][x + 1]) -
-                         (S.eta[y + 1][x - 1] - T(2) * S.eta[y][x - 1] + S.eta[y - 1][x - 1])) *
-                        T(0.5) * C.inv_dx * C.inv_dy2;
-        const T e_xxy = ((S.eta[y + 1][x + 1] - T(2) * S.eta[y + 1][x] + S.eta[y + 1][x - 1]) -
-                         (S.eta[y - 1][x + 1] - T(2) * S.eta[y - 1][x] + S.eta[y - 1][x - 1])) *
-                        T(0.5) * C.inv_dy * C.inv_dx2;
-        const T gd2 = C.g * d * d;
-        const T gd3 = gd2 * d;
-        rp += C.b_disp * gd3 * (e_xxx + e_xyy) +
-              C.b_disp * gd2 * (dx_ * (T(2) * e_xx + e_yy) + dy_ * e_xy);
-        rq += C.b_disp * gd3 * (e_yyy + e_xxy) +
-              C.b_disp * gd2 * (dy_ * (T(2) * e_yy + e_xx) + dx_ * e_xy);
-        // cross_rates (_kernels.py:310-321)
-        const T q_x = (S.q[y][x + 1] - S.q[y][x - 1]) * T(0.5) * C.inv_dx;
-        const T q_y = (S.q[y + 1][x] - S.q[y - 1][x]) * T(0.5) * C.inv_dy;
-        const T q_xy = (S.q[y + 1][x + 1] - S.q[y + 1][x - 1] - S.q[y - 1][x + 1] +
-                        S.q[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
-        const T p_x = (S.p[y][x + 1] - S.p[y][x - 1]) * T(0.5) * C.inv_dx;
-        const T p_y = (S.p[y + 1][x] - S.p[y - 1][x]) * T(0.5) * C.inv_dy;
-        const T p_xy = (S.p[y + 1][x + 1] - S.p[y + 1][x - 1] - S.p[y - 1][x + 1] +
-                        S.p[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
-        const T sixth = div_static(d, C.six, C.r_six);
-        const T d2 = C.bp13 * d * d;
-        fs_ = sixth * (dx_ * q_y + dy_ * q_x) + d2 * q_xy;
-        gs_ = sixth * (dx_ * p_y + dy_ * p_x) + d2 * p_xy;
-    } else {
-        fs_ = T(0);
-        gs_ = T(0);
-    }
-
-    // non-finite stage values (dispersion.py:92-98): first row-major cell
-    const unsigned long long lin = (unsigned long long)(J - GL) * nx + (I - GL);
-    if (!isfinite(rw)) atomicMin(&A.bad[0], lin);
-    if (!isfinite(rp)) atomicMin(&A.bad[1], lin);
-    if (!isfinite(rq)) atomicMin(&A.bad[2], lin);
-    if (!isfinite(fs_)) atomicMin(&A.bad[3], lin);
-    if (!isfinite(gs_)) atomicMin(&A.bad[4], lin);
-
-    A.h0[0][o] = rw;
-    A.h0[1][o] = rp;
-    A.h0[2][o] = rq;
-    A.h0[3][o] = fs_;
-    A.h0[4][o] = gs_;
-    if (!predict) return;
-
-    // U*, V* (dispersion.py:131-148): divisions by grid constants
-    const T p_x = div_static(S.p[y][x + 1] - S.p[y][x - 1], C.two_dx, C.r_two_dx);
-    const T p_xx = div_static(S.p[y][x + 1] - T(2) * pc + S.p[y][x - 1], C.dx2, C.r_dx2);
-    const T ustar = pc - div_static(d * dx_, C.three, C.r_three) * p_x - C.bp13 * d * d * p_xx;
-    const T q_y = div_static(S.q[y + 1][x] - S.q[y - 1][x], C.two_dy, C.r_two_dy);
-    const T q_yy = div_static(S.q[y + 1][x] - T(2) * qc + S.q[y - 1][x], C.dy2, C.r_dy2);
-    const T vstar = qc - div_static(d * dy_, C.three, C.r_three) * q_y - C.bp13 * d * d * q_yy;
-
-    // predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
-    T wn, bu, bv, us, vs;
-    if (P->euler) {
-        const T dt = T(P->dt);
-        wn = wc + dt * rw;
-        bu = ustar + dt * rp;
-        bv = vstar + dt * rq;
-        us = bu;
-        vs = bv;
-    } else {
-        const T wc0 = T(P->wc), wp1 = T(P->wp), wp2 = T(P->wp2);
-        const T s0 = T(P->sc), s1 = T(P->sp), s2 = T(P->sp2);
-        wn = wc + (wc0 * rw + wp1 * A.h1[0][o] + wp2 * A.h2[0][o]);
-        bu = ustar + (wc0 * rp + wp1 * A.h1[1][o] + wp2 * A.h2[1][o]);
-        bv = vstar + (wc0 * rq + wp1 * A.h1[2][o] + wp2 * A.h2[2][o]);
-        us = bu + (s0 * fs_ + s1 * A.h1[3][o] + s2 * A.h2[3][o]);
-        vs = bv + (s0 * gs_ + s1 * A.h1[4][o] + s2 * A.h2[4][o]);
-    }
-    A.wn[o] = wn;
-    A.bu[o] = bu;
-    A.bv[o] = bv;
-    A.us[o] = us;
-    A.vs[o] = vs;
 }
 
 template <class T>
@@ -329,8 +295,8 @@ void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A,
         cudaFuncSetAttribute(k_stage<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    dim3 grid((C.L.nx + TX - 1) / TX, (C.L.ny + TY - 1) / TY);
-    k_stage<T><<<grid, dim3(TX, TY), smem, st>>>(C, P, A, predict);
+    dim3 grid((C.L.nx + SW_ - 1) / SW_, (C.L.ny + STY - 1) / STY);
+    k_stage<T><<<grid, SW_ * SNW, smem, st>>>(C, P, A, predict);
 }
 
 template void launch_stage<double>(const Consts<double> &, const DevParams *,
