@@ -65,21 +65,36 @@ __global__ void __launch_bounds__(SW_ *SNW) k_stage(Consts<T> C, const DevParams
     const int I0 = GL + blockIdx.x * SW_, J0 = GL + blockIdx.y * STY;
 
     // ---- tile + 2-cell halo; eta = (w - bed_eff) - depth (dispersion.py:87) ----
-    for (int k = threadIdx.x; k < SHY * SHX; k += SW_ * SNW) {
-        const int y = k / SHX, x = k - y * SHX;
-        const int J = J0 - 2 + y, I = I0 - 2 + x;
-        T w = 0, p = 0, q = 0, e = 0;
-        if (J < nyt && I < nxt) {
-            const long o = L.at(J, I);
-            w = A.w[o];
-            p = A.p[o];
-            q = A.q[o];
-            e = (w - A.be[o]) - A.dep[o];
+    // batches of LB items per thread, all loads of a batch in flight together
+    constexpr int NTH = SW_ * SNW, NIT = (SHY * SHX + NTH - 1) / NTH, LB = 4;
+#pragma unroll 1
+    for (int b = 0; b < NIT; b += LB) {
+        T vw[LB], vp[LB], vq[LB], vb[LB], vd[LB];
+#pragma unroll
+        for (int u = 0; u < LB; u++) {
+            const int k = threadIdx.x + (b + u) * NTH;
+            const int y = k / SHX, x = k - y * SHX;
+            const int J = J0 - 2 + y, I = I0 - 2 + x;
+            const bool in = k < SHY * SHX && J < nyt && I < nxt;
+            const long o = in ? L.at(J, I) : L.at(GL, GL);
+            vw[u] = A.w[o];
+            vp[u] = A.p[o];
+            vq[u] = A.q[o];
+            vb[u] = A.be[o];
+            vd[u] = A.dep[o];
         }
-        S.w[y][x] = w;
-        S.p[y][x] = p;
-        S.q[y][x] = q;
-        S.eta[y][x] = e;
+#pragma unroll
+        for (int u = 0; u < LB; u++) {
+            const int k = threadIdx.x + (b + u) * NTH;
+            if (k >= SHY * SHX) continue;
+            const int y = k / SHX, x = k - y * SHX;
+            const int J = J0 - 2 + y, I = I0 - 2 + x;
+            const bool in = J < nyt && I < nxt;
+            S.w[y][x] = in ? vw[u] : T(0);
+            S.p[y][x] = in ? vp[u] : T(0);
+            S.q[y][x] = in ? vq[u] : T(0);
+            S.eta[y][x] = in ? (vw[u] - vb[u]) - vd[u] : T(0);
+        }
     }
     __syncthreads();
 
@@ -137,8 +152,23 @@ __global__ void __launch_bounds__(SW_ *SNW) k_stage(Consts<T> C, const DevParams
     }
 
     T bfx_e = bfx_at(jw, I);  // prefetch row jw's face beds
+    const bool ab3 = predict && !P->euler;
     for (int r = 0; r < SR; r++) {
         const int J = jw + r, yy = J - (J0 - 2);
+        const bool cell = J < ny + GL && I < nx + GL;
+        // issue this row's global loads first: they are consumed after the
+        // flux work, which hides their latency
+        const long o = cell ? L.at(J, I) : L.at(GL, GL);
+        const T c_be = A.be[o], c_d = A.dep[o], c_dx = A.ddx[o], c_dy = A.ddy[o];
+        const T bfy_nn = bfy_at(J + 1, I);
+        T h1v[5], h2v[5];
+        if (ab3) {
+#pragma unroll
+            for (int f = 0; f < 5; f++) {
+                h1v[f] = A.h1[f][o];
+                h2v[f] = A.h2[f][o];
+            }
+        }
         // -- x: own faces, the west flux, the east flux from the east lane --
         const T bx_e = bfx_e;                       // bed_face_x[J][I]
         T bx_w = shfl_up1(bx_e);                    // bed_face_x[J][I-1]
@@ -162,20 +192,18 @@ __global__ void __launch_bounds__(SW_ *SNW) k_stage(Consts<T> C, const DevParams
             fe_3 = g3;
         }
         // -- y: faces of row J+1, flux through the J|J+1 face (carried north) --
-        const T bfy_nn = bfy_at(J + 1, I);
         const Faces<T> yn = yfaces(yy + 1, x, bfy_nn, bfy_n);
         T fn1, fnq, fnp;
         cu_flux_rcp(yc.whi, yn.wlo, yc.qhi, yn.qlo, yc.phi, yn.plo, bfy_n, g, h_eps, fn1, fnq, fnp);
         const T fn2 = fnp, fn3 = fnq;
 
-        if (J < ny + GL && I < nx + GL) {
-            const long o = L.at(J, I);
+        if (cell) {
             const T wc = S.w[yy][x], pc = S.p[yy][x], qc = S.q[yy][x];
             // fv_rates (_kernels.py:230-251)
             T rw = -(fe_1 - fw1) * C.inv_dx - (fn1 - fs1) * C.inv_dy;
             const T src_x = -g * (wc - T(0.5) * (bx_e + bx_w)) * (bx_e - bx_w) * C.inv_dx;
             const T src_y = -g * (wc - T(0.5) * (bfy_n + bfy_s)) * (bfy_n - bfy_s) * C.inv_dy;
-            T h = wc - A.be[o];
+            T h = wc - c_be;
             if (h < T(0)) h = T(0);
             const T hstar = h > h_eps ? h : h_eps;
             T fric = T(0);
@@ -183,7 +211,7 @@ __global__ void __launch_bounds__(SW_ *SNW) k_stage(Consts<T> C, const DevParams
             T rp = -(fe_2 - fw2) * C.inv_dx - (fn2 - fs2) * C.inv_dy + src_x - fric * pc;
             T rq = -(fe_3 - fw3) * C.inv_dx - (fn3 - fs3) * C.inv_dy + src_y - fric * qc;
 
-            const T d = A.dep[o], dx_ = A.ddx[o], dy_ = A.ddy[o];
+            const T d = c_d, dx_ = c_dx, dy_ = c_dy;
             T fs_ = T(0), gs_ = T(0);
             if (d > T(0)) {
                 // dispersive_rates (_kernels.py:269-288)
@@ -263,11 +291,11 @@ __global__ void __launch_bounds__(SW_ *SNW) k_stage(Consts<T> C, const DevParams
                 } else {
                     const T wc0 = T(P->wc), wp1 = T(P->wp), wp2 = T(P->wp2);
                     const T s0 = T(P->sc), s1 = T(P->sp), s2 = T(P->sp2);
-                    wn = wc + (wc0 * rw + wp1 * A.h1[0][o] + wp2 * A.h2[0][o]);
-                    bu = ustar + (wc0 * rp + wp1 * A.h1[1][o] + wp2 * A.h2[1][o]);
-                    bv = vstar + (wc0 * rq + wp1 * A.h1[2][o] + wp2 * A.h2[2][o]);
-                    us = bu + (s0 * fs_ + s1 * A.h1[3][o] + s2 * A.h2[3][o]);
-                    vs = bv + (s0 * gs_ + s1 * A.h1[4][o] + s2 * A.h2[4][o]);
+                    wn = wc + (wc0 * rw + wp1 * h1v[0] + wp2 * h2v[0]);
+                    bu = ustar + (wc0 * rp + wp1 * h1v[1] + wp2 * h2v[1]);
+                    bv = vstar + (wc0 * rq + wp1 * h1v[2] + wp2 * h2v[2]);
+                    us = bu + (s0 * fs_ + s1 * h1v[3] + s2 * h2v[3]);
+                    vs = bv + (s0 * gs_ + s1 * h1v[4] + s2 * h2v[4]);
                 }
                 A.wn[o] = wn;
                 A.bu[o] = bu;
