@@ -42,10 +42,24 @@ constexpr int SHX = SW_ + 4, SHY = STY + 4;
 constexpr unsigned FULL = 0xffffffffu;
 static_assert(SR <= 16, "edge pre-pass uses lanes 0..SR-1 and 16..16+SR-1");
 
+// per-cell inputs a row consumes after its flux work, landed by cp.async
+enum { CI_BE, CI_D, CI_DX, CI_DY, CI_H1, CI_H2 = CI_H1 + 5, CI_N = CI_H2 + 5 };
+
 template <class T>
 struct StageSmem {
     T w[SHY][SHX], p[SHY][SHX], q[SHY][SHX], eta[SHY][SHX];
+    T cin[SNW][CI_N][SW_];  // this row's cell inputs, per warp
 };
+
+__device__ __forceinline__ void cp_async_elem(void *dst, const void *src, int bytes) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 template <class T>
 __device__ __forceinline__ T shfl_idx(T v, int src) { return __shfl_sync(FULL, v, src); }
@@ -55,7 +69,7 @@ template <class T>
 __device__ __forceinline__ T shfl_dn1(T v) { return __shfl_down_sync(FULL, v, 1); }
 
 template <class T>
-__global__ void __launch_bounds__(SW_ *SNW) k_stage(Consts<T> C, const DevParams *__restrict__ P,
+__global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevParams *__restrict__ P,
                                                    StagePtrs<T> A, int predict) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StageSmem<T> &S = *reinterpret_cast<StageSmem<T> *>(smem_raw);
@@ -156,19 +170,23 @@ __global__ void __launch_bounds__(SW_ *SNW) k_stage(Consts<T> C, const DevParams
     for (int r = 0; r < SR; r++) {
         const int J = jw + r, yy = J - (J0 - 2);
         const bool cell = J < ny + GL && I < nx + GL;
-        // issue this row's global loads first: they are consumed after the
-        // flux work, which hides their latency
+        // this row's per-cell inputs go straight to shared memory (cp.async):
+        // in flight during the flux work, holding no registers
         const long o = cell ? L.at(J, I) : L.at(GL, GL);
-        const T c_be = A.be[o], c_d = A.dep[o], c_dx = A.ddx[o], c_dy = A.ddy[o];
-        const T bfy_nn = bfy_at(J + 1, I);
-        T h1v[5], h2v[5];
+        T(*ci)[SW_] = S.cin[warp];
+        cp_async_elem(&ci[CI_BE][lane], A.be + o, sizeof(T));
+        cp_async_elem(&ci[CI_D][lane], A.dep + o, sizeof(T));
+        cp_async_elem(&ci[CI_DX][lane], A.ddx + o, sizeof(T));
+        cp_async_elem(&ci[CI_DY][lane], A.ddy + o, sizeof(T));
         if (ab3) {
 #pragma unroll
             for (int f = 0; f < 5; f++) {
-                h1v[f] = A.h1[f][o];
-                h2v[f] = A.h2[f][o];
+                cp_async_elem(&ci[CI_H1 + f][lane], A.h1[f] + o, sizeof(T));
+                cp_async_elem(&ci[CI_H2 + f][lane], A.h2[f] + o, sizeof(T));
             }
         }
+        cp_async_commit();
+        const T bfy_nn = bfy_at(J + 1, I);
         // -- x: own faces, the west flux, the east flux from the east lane --
         const T bx_e = bfx_e;                       // bed_face_x[J][I]
         T bx_w = shfl_up1(bx_e);                    // bed_face_x[J][I-1]
@@ -197,8 +215,11 @@ __global__ void __launch_bounds__(SW_ *SNW) k_stage(Consts<T> C, const DevParams
         cu_flux_rcp(yc.whi, yn.wlo, yc.qhi, yn.qlo, yc.phi, yn.plo, bfy_n, g, h_eps, fn1, fnq, fnp);
         const T fn2 = fnp, fn3 = fnq;
 
+        cp_async_wait_all();  // this lane's cell inputs have landed
         if (cell) {
             const T wc = S.w[yy][x], pc = S.p[yy][x], qc = S.q[yy][x];
+            const T c_be = ci[CI_BE][lane], c_d = ci[CI_D][lane];
+            const T c_dx = ci[CI_DX][lane], c_dy = ci[CI_DY][lane];
             // fv_rates (_kernels.py:230-251)
             T rw = -(fe_1 - fw1) * C.inv_dx - (fn1 - fs1) * C.inv_dy;
             const T src_x = -g * (wc - T(0.5) * (bx_e + bx_w)) * (bx_e - bx_w) * C.inv_dx;
@@ -291,11 +312,13 @@ __global__ void __launch_bounds__(SW_ *SNW) k_stage(Consts<T> C, const DevParams
                 } else {
                     const T wc0 = T(P->wc), wp1 = T(P->wp), wp2 = T(P->wp2);
                     const T s0 = T(P->sc), s1 = T(P->sp), s2 = T(P->sp2);
-                    wn = wc + (wc0 * rw + wp1 * h1v[0] + wp2 * h2v[0]);
-                    bu = ustar + (wc0 * rp + wp1 * h1v[1] + wp2 * h2v[1]);
-                    bv = vstar + (wc0 * rq + wp1 * h1v[2] + wp2 * h2v[2]);
-                    us = bu + (s0 * fs_ + s1 * h1v[3] + s2 * h2v[3]);
-                    vs = bv + (s0 * gs_ + s1 * h1v[4] + s2 * h2v[4]);
+                    const T(*h1v)[SW_] = &ci[CI_H1];
+                    const T(*h2v)[SW_] = &ci[CI_H2];
+                    wn = wc + (wc0 * rw + wp1 * h1v[0][lane] + wp2 * h2v[0][lane]);
+                    bu = ustar + (wc0 * rp + wp1 * h1v[1][lane] + wp2 * h2v[1][lane]);
+                    bv = vstar + (wc0 * rq + wp1 * h1v[2][lane] + wp2 * h2v[2][lane]);
+                    us = bu + (s0 * fs_ + s1 * h1v[3][lane] + s2 * h2v[3][lane]);
+                    vs = bv + (s0 * gs_ + s1 * h1v[4][lane] + s2 * h2v[4][lane]);
                 }
                 A.wn[o] = wn;
                 A.bu[o] = bu;
