@@ -28,6 +28,7 @@
 // reference, so the result is bitwise the reference's.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "bsq_device.cuh"
 #include "bsq_launch.h"
@@ -338,8 +339,20 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
 }
 
 template <class T>
+void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
+                        cudaStream_t st);
+
+// fp64 runs the tiled variant (bsq_stage_tiled.cu: 64 registers, 32 warps per
+// SM, 1.31 ms at 4096^2) -- the column walk needs 128 fp64 registers and
+// loses on latency hiding (1.35 ms); fp32 runs the column walk (71
+// registers; 1.50 vs 1.66 ms per step).  Measured A/B on B200, round 1.
+template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
                   cudaStream_t st) {
+    if constexpr (sizeof(T) == 8) {
+        launch_stage_tiled(C, P, A, predict, st);
+        return;
+    }
     const size_t smem = sizeof(StageSmem<T>);
     static bool attr_set = false;
     if (!attr_set) {

@@ -1,0 +1,307 @@
+// bsq_stage_tiled.cu -- tiled variant of the fused stage kernel: everything a step evaluates on the
+// state at t_n, in one pass over HBM.
+//
+// Per interior cell this computes the reference's
+//   faces_x/faces_y  (_kernels.py:29-103)   limited faces + positivity shift
+//   flux_x/flux_y    (_kernels.py:106-212)  central-upwind fluxes, wet/dry
+//   fv_rates         (_kernels.py:215-251)  divergence, bed source, friction
+//   eta + dispersive_rates (dispersion.py:87, _kernels.py:254-288)
+//   cross_rates      (_kernels.py:291-321)  F*, G*
+//   compute_ustar_vstar (dispersion.py:120-149)
+//   Euler / AB3 predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
+// and writes the new stage level, the predicted w, U*, V* and the
+// quadrature bases.  Faces and fluxes live only in shared memory.
+//
+// CTA = 32 x 8 cells.  Phases (each ends in __syncthreads):
+//   A  load w, P, Q (+ eta) for the tile and a 2-cell halo, and face beds
+//   B  faces of every cell once: x faces for columns -1..32, y faces for
+//      rows -1..8 of the tile (the reference evaluates each face once too)
+//   C  fluxes of the 33 x 8 x-interfaces and 32 x 9 y-interfaces, held in
+//      registers across a barrier and stored over the dead face buffers
+//   D  per-cell rates, dispersive terms, cross groups, U*/V*, predictor
+#include <cmath>
+#include <cstdint>
+
+#include "bsq_device.cuh"
+#include "bsq_launch.h"
+
+namespace bsq {
+
+namespace tiled {
+constexpr int TX = 32, TY = 8, NT = TX * TY;
+constexpr int HX = TX + 4, HY = TY + 4;       // tile + 2-cell halo
+constexpr int FXW = TX + 2, FYH = TY + 2;     // cells with x faces per row / rows with y faces
+constexpr int NXF = TY * FXW, NYF = FYH * TX; // face items
+constexpr int NXI = TY * (TX + 1), NYI = (TY + 1) * TX;  // interface items
+constexpr int NFL = NXI + NYI;
+constexpr int FL_PASSES = (NFL + NT - 1) / NT;
+
+template <class T>
+struct StageSmem {
+    T w[HY][HX], p[HY][HX], q[HY][HX], eta[HY][HX];
+    T bfx[TY][TX + 3];  // bed_face_x for columns -2..TX
+    T bfy[TY + 3][TX];  // bed_face_y for rows -2..TY
+    union {
+        struct {  // phase B/C: faces (hi = east/north, lo = west/south)
+            T xwhi[TY][FXW], xwlo[TY][FXW], xphi[TY][FXW], xplo[TY][FXW], xqhi[TY][FXW],
+                xqlo[TY][FXW];
+            T ywhi[FYH][TX], ywlo[FYH][TX], yphi[FYH][TX], yplo[FYH][TX], yqhi[FYH][TX],
+                yqlo[FYH][TX];
+        } f;
+        struct {  // phase C/D: fluxes through the tile's interfaces
+            T fx[3][TY][TX + 1];
+            T fy[3][TY + 1][TX];
+        } x;
+    } u;
+};
+
+
+template <class T>
+__global__ void __launch_bounds__(NT, 4) k_stage(Consts<T> C, const DevParams *__restrict__ P,
+                                                 StagePtrs<T> A, int predict) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    StageSmem<T> &S = *reinterpret_cast<StageSmem<T> *>(smem_raw);
+    const Layout L = C.L;
+    const int nx = L.nx, ny = L.ny, nxt = nx + 4, nyt = ny + 4;
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int I0 = GL + blockIdx.x * TX, J0 = GL + blockIdx.y * TY;
+
+    // ---- A: tile + halo ------------------------------------------------------
+    for (int k = tid; k < HY * HX; k += NT) {
+        const int y = k / HX, x = k - y * HX;
+        const int J = J0 - 2 + y, I = I0 - 2 + x;
+        T w = 0, p = 0, q = 0, e = 0;
+        if (J < nyt && I < nxt) {
+            const long o = L.at(J, I);
+            w = A.w[o];
+            p = A.p[o];
+            q = A.q[o];
+            e = (w - A.be[o]) - A.dep[o];  // dispersion.py:87
+        }
+        S.w[y][x] = w;
+        S.p[y][x] = p;
+        S.q[y][x] = q;
+        S.eta[y][x] = e;
+    }
+    for (int k = tid; k < TY * (TX + 3); k += NT) {
+        const int y = k / (TX + 3), x = k - y * (TX + 3);
+        const int J = J0 + y, I = I0 - 2 + x;
+        S.bfx[y][x] = (J < nyt && I <= nx + 2) ? A.bfx[L.at(J, I)] : T(0);
+    }
+    for (int k = tid; k < (TY + 3) * TX; k += NT) {
+        const int y = k / TX, x = k - y * TX;
+        const int J = J0 - 2 + y, I = I0 + x;
+        S.bfy[y][x] = (J <= ny + 2 && I < nxt) ? A.bfy[L.at(J, I)] : T(0);
+    }
+    __syncthreads();
+
+    // ---- B: faces, once per cell ------------------------------------------------
+    for (int k = tid; k < NXF + NYF; k += NT) {
+        if (k < NXF) {  // x faces of cell (row r, column c-1), c = 0..TX+1
+            const int r = k / FXW, c = k - r * FXW;
+            const int y = r + 2, x = c + 1;  // smem coords of the cell
+            const Faces<T> f = cell_faces(S.w[y][x - 1], S.w[y][x], S.w[y][x + 1], S.p[y][x - 1],
+                                          S.p[y][x], S.p[y][x + 1], S.q[y][x - 1], S.q[y][x],
+                                          S.q[y][x + 1], S.bfx[r][c + 1], S.bfx[r][c], C.theta);
+            S.u.f.xwhi[r][c] = f.whi;
+            S.u.f.xwlo[r][c] = f.wlo;
+            S.u.f.xphi[r][c] = f.phi;
+            S.u.f.xplo[r][c] = f.plo;
+            S.u.f.xqhi[r][c] = f.qhi;
+            S.u.f.xqlo[r][c] = f.qlo;
+        } else {  // y faces of cell (row r-1, column c), r = 0..TY+1
+            const int kk = k - NXF;
+            const int r = kk / TX, c = kk - r * TX;
+            const int y = r + 1, x = c + 2;
+            const Faces<T> f = cell_faces(S.w[y - 1][x], S.w[y][x], S.w[y + 1][x], S.p[y - 1][x],
+                                          S.p[y][x], S.p[y + 1][x], S.q[y - 1][x], S.q[y][x],
+                                          S.q[y + 1][x], S.bfy[r + 1][c], S.bfy[r][c], C.theta);
+            S.u.f.ywhi[r][c] = f.whi;
+            S.u.f.ywlo[r][c] = f.wlo;
+            S.u.f.yphi[r][c] = f.phi;
+            S.u.f.yplo[r][c] = f.plo;
+            S.u.f.yqhi[r][c] = f.qhi;
+            S.u.f.yqlo[r][c] = f.qlo;
+        }
+    }
+    __syncthreads();
+
+    // ---- C: fluxes (registers across the barrier, then over the faces) ----------
+    T fl[FL_PASSES][3];
+#pragma unroll
+    for (int s = 0; s < FL_PASSES; s++) {
+        const int k = tid + s * NT;
+        if (k < NXI) {  // interface between tile columns xi-1 and xi, row r
+            const int r = k / (TX + 1), xi = k - r * (TX + 1);
+            // left cell = face column xi, right cell = face column xi+1
+            cu_flux_rcp(S.u.f.xwhi[r][xi], S.u.f.xwlo[r][xi + 1], S.u.f.xphi[r][xi],
+                        S.u.f.xplo[r][xi + 1], S.u.f.xqhi[r][xi], S.u.f.xqlo[r][xi + 1],
+                        S.bfx[r][xi + 1], C.g, C.h_eps, fl[s][0], fl[s][1], fl[s][2]);
+        } else if (k < NFL) {  // interface between tile rows yi-1 and yi, column c
+            const int kk = k - NXI;
+            const int yi = kk / TX, c = kk - yi * TX;
+            // south cell = face row yi, north cell = face row yi+1; normal = Q
+            T f1, fq, fp;
+            cu_flux_rcp(S.u.f.ywhi[yi][c], S.u.f.ywlo[yi + 1][c], S.u.f.yqhi[yi][c],
+                        S.u.f.yqlo[yi + 1][c], S.u.f.yphi[yi][c], S.u.f.yplo[yi + 1][c],
+                        S.bfy[yi + 1][c], C.g, C.h_eps, f1, fq, fp);
+            fl[s][0] = f1;
+            fl[s][1] = fp;  // fy2 carries P
+            fl[s][2] = fq;  // fy3 carries Q
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < FL_PASSES; s++) {
+        const int k = tid + s * NT;
+        if (k < NXI) {
+            const int r = k / (TX + 1), xi = k - r * (TX + 1);
+            S.u.x.fx[0][r][xi] = fl[s][0];
+            S.u.x.fx[1][r][xi] = fl[s][1];
+            S.u.x.fx[2][r][xi] = fl[s][2];
+        } else if (k < NFL) {
+            const int kk = k - NXI;
+            const int yi = kk / TX, c = kk - yi * TX;
+            S.u.x.fy[0][yi][c] = fl[s][0];
+            S.u.x.fy[1][yi][c] = fl[s][1];
+            S.u.x.fy[2][yi][c] = fl[s][2];
+        }
+    }
+    __syncthreads();
+
+    // ---- D: per cell ----------------------------------------------------------------
+    const int J = J0 + ty, I = I0 + tx;
+    if (J >= ny + GL || I >= nx + GL) return;
+    const int y = ty + 2, x = tx + 2;
+    const long o = L.at(J, I);
+    const T wc = S.w[y][x], pc = S.p[y][x], qc = S.q[y][x];
+    const T be_ = S.bfx[ty][tx + 2], bw_ = S.bfx[ty][tx + 1];
+    const T bn_ = S.bfy[ty + 2][tx], bs_ = S.bfy[ty + 1][tx];
+
+    // fv_rates (_kernels.py:230-251)
+    T rw = -(S.u.x.fx[0][ty][tx + 1] - S.u.x.fx[0][ty][tx]) * C.inv_dx -
+           (S.u.x.fy[0][ty + 1][tx] - S.u.x.fy[0][ty][tx]) * C.inv_dy;
+    const T src_x = -C.g * (wc - T(0.5) * (be_ + bw_)) * (be_ - bw_) * C.inv_dx;
+    const T src_y = -C.g * (wc - T(0.5) * (bn_ + bs_)) * (bn_ - bs_) * C.inv_dy;
+    T h = wc - A.be[o];
+    if (h < T(0)) h = T(0);
+    const T hstar = h > C.h_eps ? h : C.h_eps;
+    T fric = T(0);
+    if (C.c_f > T(0)) fric = C.c_f * sqrt(pc * pc + qc * qc) / (hstar * hstar);
+    T rp = -(S.u.x.fx[1][ty][tx + 1] - S.u.x.fx[1][ty][tx]) * C.inv_dx -
+           (S.u.x.fy[1][ty + 1][tx] - S.u.x.fy[1][ty][tx]) * C.inv_dy + src_x - fric * pc;
+    T rq = -(S.u.x.fx[2][ty][tx + 1] - S.u.x.fx[2][ty][tx]) * C.inv_dx -
+           (S.u.x.fy[2][ty + 1][tx] - S.u.x.fy[2][ty][tx]) * C.inv_dy + src_y - fric * qc;
+
+    const T d = A.dep[o], dx_ = A.ddx[o], dy_ = A.ddy[o];
+    T fs_, gs_;
+    if (d > T(0)) {
+        // dispersive_rates (_kernels.py:269-288)
+        const T ec = S.eta[y][x];
+        const T e_xx = (S.eta[y][x + 1] - T(2) * ec + S.eta[y][x - 1]) * C.inv_dx2;
+        const T e_yy = (S.eta[y + 1][x] - T(2) * ec + S.eta[y - 1][x]) * C.inv_dy2;
+        const T e_xy = (S.eta[y + 1][x + 1] - S.eta[y + 1][x - 1] - S.eta[y - 1][x + 1] +
+                        S.eta[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+        const T e_xxx = (S.eta[y][x + 2] - T(2) * S.eta[y][x + 1] + T(2) * S.eta[y][x - 1] -
+                         S.eta[y][x - 2]) * T(0.5) * C.inv_dx * C.inv_dx2;
+        const T e_yyy = (S.eta[y + 2][x] - T(2) * S.eta[y + 1][x] + T(2) * S.eta[y - 1][x] -
+                         S.eta[y - 2][x]) * T(0.5) * C.inv_dy * C.inv_dy2;
+        const T e_xyy = ((S.eta[y + 1][x + 1] - T(2) * S.eta[y][x + 1] + S.eta[y - 1][x + 1]) -
+                         (S.eta[y + 1][x - 1] - T(2) * S.eta[y][x - 1] + S.eta[y - 1][x - 1])) *
+                        T(0.5) * C.inv_dx * C.inv_dy2;
+        const T e_xxy = ((S.eta[y + 1][x + 1] - T(2) * S.eta[y + 1][x] + S.eta[y + 1][x - 1]) -
+                         (S.eta[y - 1][x + 1] - T(2) * S.eta[y - 1][x] + S.eta[y - 1][x - 1])) *
+                        T(0.5) * C.inv_dy * C.inv_dx2;
+        const T gd2 = C.g * d * d;
+        const T gd3 = gd2 * d;
+        rp += C.b_disp * gd3 * (e_xxx + e_xyy) +
+              C.b_disp * gd2 * (dx_ * (T(2) * e_xx + e_yy) + dy_ * e_xy);
+        rq += C.b_disp * gd3 * (e_yyy + e_xxy) +
+              C.b_disp * gd2 * (dy_ * (T(2) * e_yy + e_xx) + dx_ * e_xy);
+        // cross_rates (_kernels.py:310-321)
+        const T q_x = (S.q[y][x + 1] - S.q[y][x - 1]) * T(0.5) * C.inv_dx;
+        const T q_y = (S.q[y + 1][x] - S.q[y - 1][x]) * T(0.5) * C.inv_dy;
+        const T q_xy = (S.q[y + 1][x + 1] - S.q[y + 1][x - 1] - S.q[y - 1][x + 1] +
+                        S.q[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+        const T p_x = (S.p[y][x + 1] - S.p[y][x - 1]) * T(0.5) * C.inv_dx;
+        const T p_y = (S.p[y + 1][x] - S.p[y - 1][x]) * T(0.5) * C.inv_dy;
+        const T p_xy = (S.p[y + 1][x + 1] - S.p[y + 1][x - 1] - S.p[y - 1][x + 1] +
+                        S.p[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+        const T sixth = div_static(d, C.six, C.r_six);
+        const T d2 = C.bp13 * d * d;
+        fs_ = sixth * (dx_ * q_y + dy_ * q_x) + d2 * q_xy;
+        gs_ = sixth * (dx_ * p_y + dy_ * p_x) + d2 * p_xy;
+    } else {
+        fs_ = T(0);
+        gs_ = T(0);
+    }
+
+    // non-finite stage values (dispersion.py:92-98): first row-major cell
+    const unsigned long long lin = (unsigned long long)(J - GL) * nx + (I - GL);
+    if (!isfinite(rw)) atomicMin(&A.bad[0], lin);
+    if (!isfinite(rp)) atomicMin(&A.bad[1], lin);
+    if (!isfinite(rq)) atomicMin(&A.bad[2], lin);
+    if (!isfinite(fs_)) atomicMin(&A.bad[3], lin);
+    if (!isfinite(gs_)) atomicMin(&A.bad[4], lin);
+
+    A.h0[0][o] = rw;
+    A.h0[1][o] = rp;
+    A.h0[2][o] = rq;
+    A.h0[3][o] = fs_;
+    A.h0[4][o] = gs_;
+    if (!predict) return;
+
+    // U*, V* (dispersion.py:131-148): divisions by grid constants
+    const T p_x = div_static(S.p[y][x + 1] - S.p[y][x - 1], C.two_dx, C.r_two_dx);
+    const T p_xx = div_static(S.p[y][x + 1] - T(2) * pc + S.p[y][x - 1], C.dx2, C.r_dx2);
+    const T ustar = pc - div_static(d * dx_, C.three, C.r_three) * p_x - C.bp13 * d * d * p_xx;
+    const T q_y = div_static(S.q[y + 1][x] - S.q[y - 1][x], C.two_dy, C.r_two_dy);
+    const T q_yy = div_static(S.q[y + 1][x] - T(2) * qc + S.q[y - 1][x], C.dy2, C.r_dy2);
+    const T vstar = qc - div_static(d * dy_, C.three, C.r_three) * q_y - C.bp13 * d * d * q_yy;
+
+    // predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
+    T wn, bu, bv, us, vs;
+    if (P->euler) {
+        const T dt = T(P->dt);
+        wn = wc + dt * rw;
+        bu = ustar + dt * rp;
+        bv = vstar + dt * rq;
+        us = bu;
+        vs = bv;
+    } else {
+        const T wc0 = T(P->wc), wp1 = T(P->wp), wp2 = T(P->wp2);
+        const T s0 = T(P->sc), s1 = T(P->sp), s2 = T(P->sp2);
+        wn = wc + (wc0 * rw + wp1 * A.h1[0][o] + wp2 * A.h2[0][o]);
+        bu = ustar + (wc0 * rp + wp1 * A.h1[1][o] + wp2 * A.h2[1][o]);
+        bv = vstar + (wc0 * rq + wp1 * A.h1[2][o] + wp2 * A.h2[2][o]);
+        us = bu + (s0 * fs_ + s1 * A.h1[3][o] + s2 * A.h2[3][o]);
+        vs = bv + (s0 * gs_ + s1 * A.h1[4][o] + s2 * A.h2[4][o]);
+    }
+    A.wn[o] = wn;
+    A.bu[o] = bu;
+    A.bv[o] = bv;
+    A.us[o] = us;
+    A.vs[o] = vs;
+}
+
+}  // namespace tiled
+
+template <class T>
+void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
+                        cudaStream_t st) {
+    const size_t smem = sizeof(tiled::StageSmem<T>);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(tiled::k_stage<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    dim3 grid((C.L.nx + tiled::TX - 1) / tiled::TX, (C.L.ny + tiled::TY - 1) / tiled::TY);
+    tiled::k_stage<T><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, A, predict);
+}
+
+template void launch_stage_tiled<double>(const Consts<double> &, const DevParams *,
+                                         const StagePtrs<double> &, int, cudaStream_t);
+template void launch_stage_tiled<float>(const Consts<float> &, const DevParams *,
+                                        const StagePtrs<float> &, int, cudaStream_t);
+
+}  // namespace bsq
