@@ -436,13 +436,13 @@ static int cr_one(int n, int n2, const double *dl, const double *dd, const doubl
     }
     int i1 = n2 / 2 - 1, i2 = n2 - 1;
     double det = b[i1] * b[i2] - c[i1] * a[i2];
-    if (det == 0.0) return -1;
+    if (det == 0.0) return -2;
     x[i1] = (r[i1] * b[i2] - c[i1] * r[i2]) / det;
     x[i2] = (b[i1] * r[i2] - a[i2] * r[i1]) / det;
     stride = n2 / 4;
     while (stride >= 1) {
         for (int idx = stride - 1; idx < n2; idx += 2 * stride) {
-            if (b[idx] == 0.0) return -1;
+            if (b[idx] == 0.0) return -3;
             double lower = idx - stride >= 0 ? x[idx - stride] : 0.0;
             x[idx] = (r[idx] - a[idx] * lower - c[idx] * x[idx + stride]) / b[idx];
         }
@@ -458,22 +458,27 @@ int orc_cr_batch(int m, int n, const double *dl, const double *dd, const double 
     int n2 = 1;
     while (n2 < n) n2 *= 2;
     if (n2 < 2) n2 = 2;
-    int bad = 0;
+    /* the reference raises at the first failing line: keep the lowest k */
+    int bad_k = m, bad_rc = 0;
 #pragma omp parallel
     {
         double *buf = (double *)malloc(sizeof(double) * 5 * (size_t)n2);
 #pragma omp for schedule(static)
         for (int k = 0; k < m; k++) {
             long o = (long)k * n;
-            if (cr_one(n, n2, dl + o, dd + o, du + o, rhs + o, out + o, buf, buf + n2,
-                       buf + 2 * n2, buf + 3 * n2, buf + 4 * n2)) {
-#pragma omp atomic write
-                bad = 1;
+            int rc = cr_one(n, n2, dl + o, dd + o, du + o, rhs + o, out + o, buf, buf + n2,
+                            buf + 2 * n2, buf + 3 * n2, buf + 4 * n2);
+            if (rc) {
+#pragma omp critical(orc_cr_bad)
+                if (k < bad_k) {
+                    bad_k = k;
+                    bad_rc = rc;
+                }
             }
         }
         free(buf);
     }
-    return bad ? -1 : 0;
+    return bad_rc;
 }
 
 /* ------------------------------------------------------------------ */
@@ -711,7 +716,8 @@ static int solve_momentum(orc_sim *s, const double *us, const double *vs, const 
         s->tmp_t[(long)jj * nx] -= s->ax[(long)jj * nx] * pg_w[jj];
         s->tmp_t[(long)jj * nx + nx - 1] -= s->cx[(long)jj * nx + nx - 1] * pg_e[jj];
     }
-    if (solver(ny, nx, s->ax, s->bx, s->cx, s->tmp_t, p_out)) return -1;
+    int rc = solver(ny, nx, s->ax, s->bx, s->cx, s->tmp_t, p_out);
+    if (rc) return rc;
     /* y: transposed */
     for (int jj = 0; jj < ny; jj++)
         for (int ii = 0; ii < nx; ii++) s->tmp_t[(long)ii * ny + jj] = vs[(long)jj * nx + ii];
@@ -719,7 +725,8 @@ static int solve_momentum(orc_sim *s, const double *us, const double *vs, const 
         s->tmp_t[(long)ii * ny] -= s->ay_t[(long)ii * ny] * qg_s[ii];
         s->tmp_t[(long)ii * ny + ny - 1] -= s->cy_t[(long)ii * ny + ny - 1] * qg_n[ii];
     }
-    if (solver(nx, ny, s->ay_t, s->by_t, s->cy_t, s->tmp_t, s->out_t)) return -1;
+    rc = solver(nx, ny, s->ay_t, s->by_t, s->cy_t, s->tmp_t, s->out_t);
+    if (rc) return rc;
     for (int jj = 0; jj < ny; jj++)
         for (int ii = 0; ii < nx; ii++) q_out[(long)jj * nx + ii] = s->out_t[(long)ii * ny + jj];
     return 0;
@@ -728,8 +735,10 @@ static int solve_momentum(orc_sim *s, const double *us, const double *vs, const 
 /*
  * One step into the pending buffers (stepper.py:225-305 minus the host-side
  * controller).  Returns 0 on success, 1 if a stage value is non-finite (the
- * reference raises before pushing history: nothing is pending), -1 on a
- * zero pivot.  The caller commits with orc_commit.
+ * reference raises before pushing history: nothing is pending), or the
+ * solver's error code: -1 a zero pivot (Thomas) / zero pivot in reduction
+ * (CR), -2 a zero CR core determinant, -3 a zero pivot in CR back
+ * substitution.  The caller commits with orc_commit.
  */
 int orc_step(orc_sim *s, const orc_params *pr, orc_result *res)
 {
@@ -855,7 +864,7 @@ int orc_step(orc_sim *s, const orc_params *pr, orc_result *res)
         rc = solve_momentum(s, s->us, s->vs, pgw, pge, qgs, qgn, s->p1, s->q1);
     }
     free(pgw); free(pge); free(qgs); free(qgn);
-    if (rc) return -1;
+    if (rc) return rc; /* -1 zero pivot / reduction, -2 core determinant, -3 back substitution */
 
     /* 8. clamp, set momenta, film cutoff (stepper.py:281-292) */
     double *rowsum = (double *)malloc(sizeof(double) * ny);

@@ -45,6 +45,7 @@ enum Arr {
     A_BE, A_DEP, A_DDX, A_DDY, A_BFX, A_BFY,
     A_AX, A_DENX, A_RDENX, A_CWX, A_AY, A_DENY, A_RDENY, A_CWY,
     A_BU, A_BV, A_US, A_VS, A_P2, A_Q2,
+    A_BX, A_CX, A_BY, A_CY,  // diagonals for solver="cr"
     A_HIST0,  // 4 slots x 5 fields follow
     A_COUNT = A_HIST0 + 20
 };
@@ -92,7 +93,16 @@ int check_desc(const bsq_desc *d) {
     if (d->nx < 5 || d->ny < 5) return fail(BSQ_ERR_BAD_ARG, "grid needs at least 5x5 cells");
     if (d->precision != BSQ_FP64 && d->precision != BSQ_FP32)
         return fail(BSQ_ERR_BAD_ARG, "precision must be BSQ_FP64 or BSQ_FP32");
-    if (d->solver != BSQ_THOMAS) return fail(BSQ_ERR_BAD_ARG, "only the Thomas solver is built");
+    if (d->solver != BSQ_THOMAS && d->solver != BSQ_CR)
+        return fail(BSQ_ERR_BAD_ARG, "solver must be BSQ_THOMAS or BSQ_CR");
+    if (d->solver == BSQ_CR) {
+        if (d->south_internal || d->north_internal)
+            return fail(BSQ_ERR_BAD_ARG, "solver=cr is not sharded (use the Thomas pipeline)");
+        const int eb = d->precision == BSQ_FP64 ? 8 : 4;
+        if (cr_smem_bytes(d->nx, d->ny, eb) > 227 * 1024)
+            return fail(BSQ_ERR_BAD_ARG, "solver=cr holds a line in shared memory: lines up to "
+                                         "4096 (fp64) / 8192 (fp32) cells");
+    }
     if (!(d->dx > 0 && d->dy > 0)) return fail(BSQ_ERR_BAD_ARG, "cell sizes must be positive");
     if (d->south_internal || d->north_internal) {
         if (d->row0 < 0 || d->row0 + d->ny > d->ny_global)
@@ -280,6 +290,7 @@ struct Engine : EngineBase {
         const int nx = d.nx, ny = d.ny, nxt = nx + 4;
         const long E = L.elems();
         std::vector<T> ax(E, T(0)), denx(E, T(1)), rdenx(E, T(-1)), cwx(E, T(0));
+        std::vector<T> bxv(E, T(1)), cxv(E, T(0)), byv(E, T(1)), cyv(E, T(0));  // for "cr"
         std::vector<T> ay(E, T(0)), deny(E, T(1)), rdeny(E, T(-1)), cwy(E, T(0));
         std::vector<T> cxl(ny), cyl(nx);
         const double six_dx = 6.0 * d.dx, six_dy = 6.0 * d.dy;
@@ -303,6 +314,8 @@ struct Engine : EngineBase {
                 const double den = i == 0 ? b : b - a * cw_prev;
                 const double cw = cc / den;
                 put(ax, denx, rdenx, cwx, L.at(j + GL, i + GL), a, den, cw);
+                bxv[L.at(j + GL, i + GL)] = T(b);
+                cxv[L.at(j + GL, i + GL)] = T(cc);
                 cw_prev = cw;
                 if (i == nx - 1) cxl[j] = T(cc);
             }
@@ -322,6 +335,8 @@ struct Engine : EngineBase {
                 const double den = (j == 0 && !cont) ? b : b - a * cw_prev;
                 const double cw = cc / den;
                 put(ay, deny, rdeny, cwy, L.at(j + GL, i + GL), a, den, cw);
+                byv[L.at(j + GL, i + GL)] = T(b);
+                cyv[L.at(j + GL, i + GL)] = T(cc);
                 cw_prev = cw;
                 if (j == ny - 1) cyl[i] = T(cc);
             }
@@ -330,9 +345,11 @@ struct Engine : EngineBase {
         singular = sing;
         pos_pivots = pos;
         const size_t B = sizeof(T) * E;
-        const std::vector<T> *src[8] = {&ax, &denx, &rdenx, &cwx, &ay, &deny, &rdeny, &cwy};
-        const int dst[8] = {A_AX, A_DENX, A_RDENX, A_CWX, A_AY, A_DENY, A_RDENY, A_CWY};
-        for (int k = 0; k < 8; k++)
+        const std::vector<T> *src[12] = {&ax, &denx, &rdenx, &cwx, &ay, &deny, &rdeny, &cwy,
+                                         &bxv, &cxv, &byv, &cyv};
+        const int dst[12] = {A_AX, A_DENX, A_RDENX, A_CWX, A_AY, A_DENY, A_RDENY, A_CWY,
+                             A_BX, A_CX, A_BY, A_CY};
+        for (int k = 0; k < (d.solver == BSQ_CR ? 12 : 8); k++)
             CU(cudaMemcpyAsync(arr[dst[k]], src[k]->data(), B, cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(cx_last, cxl.data(), sizeof(T) * ny, cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(cy_last, cyl.data(), sizeof(T) * nx, cudaMemcpyHostToDevice, st));
@@ -601,7 +618,10 @@ struct Engine : EngineBase {
             ev_mark("ghost_n");
             break;
         case BSQ_PH_SOLVE1F:
-            launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st, fwd_mode);
+            if (d.solver == BSQ_CR)
+                launch_cr(C, cr_ptrs(1, nxt), st);
+            else
+                launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st, fwd_mode);
             ev_mark("solve1");
             break;
         case BSQ_PH_SOLVE1B:
@@ -618,7 +638,10 @@ struct Engine : EngineBase {
             break;
         case BSQ_PH_SOLVE2F:
             if (d.cross_correction) {
-                launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st, fwd_mode);
+                if (d.solver == BSQ_CR)
+                    launch_cr(C, cr_ptrs(2, nxt), st);
+                else
+                    launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st, fwd_mode);
                 ev_mark("solve2");
             }
             break;
@@ -671,8 +694,40 @@ struct Engine : EngineBase {
         pending = true;
         bool stage_err = false;
         for (int k = 0; k < 5; k++) stage_err |= r->stage_bad[k] >= 0;
-        if (singular && !stage_err) return fail(BSQ_ERR_SINGULAR, "singular tridiagonal system: zero pivot");
+        if (stage_err) return BSQ_OK;  // the stage error is raised first (dispersion.py:92-98)
+        if (d.solver == BSQ_CR && hres->cr_bad != 0xFFFFFFFFu) {
+            return fail(BSQ_ERR_SINGULAR, cr_message(hres->cr_bad));
+        }
+        if (d.solver != BSQ_CR && singular)
+            return fail(BSQ_ERR_SINGULAR, "singular tridiagonal system: zero pivot");
         return BSQ_OK;
+    }
+
+    // the ZeroDivisionError text of cyclic_reduction_batch (_kernels.py:419-446)
+    static const char *cr_message(unsigned key) {
+        static const char *msg[3] = {"singular tridiagonal system in reduction",
+                                     "singular tridiagonal system: zero core determinant",
+                                     "singular tridiagonal system in back substitution"};
+        return msg[(key & 3u) < 3u ? (key & 3u) : 0];
+    }
+
+    CrPtrs<T> cr_ptrs(int phase, int nxt_state) {
+        CrPtrs<T> K;
+        K.ax = arr[A_AX];
+        K.bx = arr[A_BX];
+        K.cx = arr[A_CX];
+        K.ay = arr[A_AY];
+        K.by = arr[A_BY];
+        K.cy = arr[A_CY];
+        K.rx = arr[A_US];
+        K.ry = arr[A_VS];
+        K.gp = Pp(nxt_state);
+        K.gq = Qq(nxt_state);
+        K.outx = phase == 1 ? Pp(nxt_state) : arr[A_P2];
+        K.outy = phase == 1 ? Qq(nxt_state) : arr[A_Q2];
+        K.bad = &dres->cr_bad;
+        K.key_base = phase == 1 ? 0u : 1u << 31;
+        return K;
     }
 
     int array_layout(int which, size_t *off, int *pitch, int *xo, int *eb) {
@@ -722,7 +777,8 @@ struct Engine : EngineBase {
 
     int solve_momentum(const double *us, const double *vs, const double *pgw, const double *pge,
                        const double *qgs, const double *qgn, double *pout, double *qout) {
-        if (singular) return fail(BSQ_ERR_SINGULAR, "singular tridiagonal system: zero pivot");
+        if (d.solver != BSQ_CR && singular)
+            return fail(BSQ_ERR_SINGULAR, "singular tridiagonal system: zero pivot");
         const int nxt = 1 - cur, nx = d.nx, ny = d.ny;
         int rc;
         if ((rc = upload_interior(arr[A_US], us)) || (rc = upload_interior(arr[A_VS], vs)))
@@ -733,12 +789,20 @@ struct Engine : EngineBase {
             (rc = upload(Qq(nxt), L.at(GL - 1, GL), qgs, 1, nx, nx)) ||
             (rc = upload(Qq(nxt), L.at(ny + GL, GL), qgn, 1, nx, nx)))
             return rc;
-        launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st);  // into P2 / Q2
+        if (d.solver == BSQ_CR) {
+            CU(cudaMemsetAsync(&dres->cr_bad, 0xFF, sizeof(unsigned int), st));
+            launch_cr(C, cr_ptrs(2, nxt), st);  // into P2 / Q2
+        } else {
+            launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st);
+        }
         CU(cudaGetLastError());
         if ((rc = download_interior(pout, arr[A_P2])) || (rc = download_interior(qout, arr[A_Q2])))
             return rc;
+        CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
         pending = false;
+        if (d.solver == BSQ_CR && hres->cr_bad != 0xFFFFFFFFu)
+            return fail(BSQ_ERR_SINGULAR, cr_message(hres->cr_bad));
         return BSQ_OK;
     }
 

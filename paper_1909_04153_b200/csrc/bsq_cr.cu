@@ -1,0 +1,150 @@
+// bsq_cr.cu -- the reference's optional odd-even cyclic-reduction line
+// solver (solver="cr": cyclic_reduction_batch, _kernels.py:384-451), one CTA
+// per line, the line held in shared memory.
+//
+// Within one reduction level the reference updates the rows
+// idx = 2s-1, 4s-1, ... from rows idx -/+ s, which that level does not
+// modify; within one back-substitution level it fills rows s-1, 3s-1, ...
+// from rows already solved at coarser levels.  Each level is therefore a
+// data-parallel map over idx, and running it with one thread per idx (a
+// barrier between levels) performs exactly the reference's operations:
+// results are bitwise equal.  Divisions are by per-row values (IEEE `/`).
+// A zero pivot records (atomicMin) the key of the error the reference would
+// raise first -- solve phase, x before y, line, then reduction / core /
+// back substitution -- so the host reports the same ZeroDivisionError.
+#include <cstdint>
+
+#include "bsq_device.cuh"
+#include "bsq_launch.h"
+
+namespace bsq {
+
+constexpr int CR_THREADS = 512;
+
+// line l of direction xdir: element e at padded (GL+l, GL+e) (x) or
+// (GL+e, GL+l) (y)
+template <class T, bool XDIR>
+__device__ void cr_line(const Consts<T> &C, const CrPtrs<T> &K, int line, T *sm, int n2) {
+    const Layout L = C.L;
+    const int n = XDIR ? L.nx : L.ny;
+    T *a = sm, *b = sm + n2, *c = sm + 2 * n2, *r = sm + 3 * n2, *x = sm + 4 * n2;
+    const T *A = XDIR ? K.ax : K.ay;
+    const T *B = XDIR ? K.bx : K.by;
+    const T *Cc = XDIR ? K.cx : K.cy;
+    const T *R = XDIR ? K.rx : K.ry;
+    auto off = [&](int e) -> long { return XDIR ? L.at(GL + line, GL + e) : L.at(GL + e, GL + line); };
+    // load + ghost folding (implicit.py:178-179 / :190-191), identity padding
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        if (i < n) {
+            const long o = off(i);
+            T rv = R[o];
+            if (i == 0) {
+                const T g0 = XDIR ? K.gp[L.at(GL + line, GL - 1)] : K.gq[L.at(GL - 1, GL + line)];
+                rv = rv - A[o] * g0;
+            }
+            if (i == n - 1) {
+                const T g1 = XDIR ? K.gp[L.at(GL + line, n + GL)] : K.gq[L.at(n + GL, GL + line)];
+                rv = rv - Cc[o] * g1;
+            }
+            a[i] = A[o];
+            b[i] = B[o];
+            c[i] = Cc[o];
+            r[i] = rv;
+        } else {
+            a[i] = T(0);
+            b[i] = T(1);
+            c[i] = T(0);
+            r[i] = T(0);
+        }
+    }
+    __syncthreads();
+    unsigned kind = 3;  // 0 reduction, 1 core determinant, 2 back substitution
+    // reduction (_kernels.py:414-434)
+    for (int stride = 1; stride < n2 / 2; stride *= 2) {
+        const int step = 2 * stride;
+        for (int k = threadIdx.x; k < n2 / step; k += blockDim.x) {
+            const int idx = step * k + step - 1;
+            const int il = idx - stride;
+            if (b[il] == T(0)) kind = 0;
+            const T alpha = -a[idx] / b[il];
+            T aa = alpha * a[il];
+            T bb = b[idx] + alpha * c[il];
+            T rr = r[idx] + alpha * r[il];
+            T cc;
+            const int ir = idx + stride;
+            if (ir < n2) {
+                if (b[ir] == T(0)) kind = 0;
+                const T beta = -c[idx] / b[ir];
+                cc = beta * c[ir];
+                bb = bb + beta * a[ir];
+                rr = rr + beta * r[ir];
+            } else {
+                cc = T(0);
+            }
+            a[idx] = aa;
+            b[idx] = bb;
+            c[idx] = cc;
+            r[idx] = rr;
+        }
+        __syncthreads();
+    }
+    // 2x2 core (_kernels.py:435-441)
+    if (threadIdx.x == 0) {
+        const int i1 = n2 / 2 - 1, i2 = n2 - 1;
+        const T det = b[i1] * b[i2] - c[i1] * a[i2];
+        if (det == T(0) && kind > 1) kind = 1;
+        x[i1] = (r[i1] * b[i2] - c[i1] * r[i2]) / det;
+        x[i2] = (b[i1] * r[i2] - a[i2] * r[i1]) / det;
+    }
+    __syncthreads();
+    // back substitution (_kernels.py:442-449)
+    for (int stride = n2 / 4; stride >= 1; stride /= 2) {
+        const int step = 2 * stride;
+        for (int k = threadIdx.x; k * step + stride - 1 < n2; k += blockDim.x) {
+            const int idx = step * k + stride - 1;
+            if (b[idx] == T(0) && kind > 2) kind = 2;
+            const T lower = idx - stride >= 0 ? x[idx - stride] : T(0);
+            x[idx] = (r[idx] - a[idx] * lower - c[idx] * x[idx + stride]) / b[idx];
+        }
+        __syncthreads();
+    }
+    if (kind < 3)
+        atomicMin(K.bad, K.key_base | (XDIR ? 0u : 1u << 30) | ((unsigned)line << 2) | kind);
+    T *out = XDIR ? K.outx : K.outy;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[off(i)] = x[i];
+}
+
+template <class T>
+__global__ void __launch_bounds__(CR_THREADS) k_cr(Consts<T> C, CrPtrs<T> K, int nbx, int n2x,
+                                                   int n2y) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *sm = reinterpret_cast<T *>(smem_raw);
+    if ((int)blockIdx.x < nbx)
+        cr_line<T, true>(C, K, blockIdx.x, sm, n2x);
+    else
+        cr_line<T, false>(C, K, blockIdx.x - nbx, sm, n2y);
+}
+
+static int pow2_at_least(int n) {
+    int n2 = 1;
+    while (n2 < n) n2 *= 2;
+    return n2 < 2 ? 2 : n2;
+}
+
+size_t cr_smem_bytes(int nx, int ny, int elem) {
+    const int n2 = pow2_at_least(nx > ny ? nx : ny);
+    return (size_t)5 * n2 * elem;
+}
+
+template <class T>
+void launch_cr(const Consts<T> &C, const CrPtrs<T> &K, cudaStream_t st) {
+    const int n2x = pow2_at_least(C.L.nx), n2y = pow2_at_least(C.L.ny);
+    const size_t smem = cr_smem_bytes(C.L.nx, C.L.ny, sizeof(T));
+    cudaFuncSetAttribute(k_cr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cr<T><<<C.L.ny + C.L.nx, CR_THREADS, smem, st>>>(C, K, C.L.ny, n2x, n2y);
+}
+
+template void launch_cr<double>(const Consts<double> &, const CrPtrs<double> &, cudaStream_t);
+template void launch_cr<float>(const Consts<float> &, const CrPtrs<float> &, cudaStream_t);
+
+}  // namespace bsq

@@ -43,6 +43,17 @@ struct SolveMaps {
     CUtensorMap y_rhs, y_a, y_den, y_rden, y_cw, y_out;
 };
 
+// solver="cr": the reference's odd-even cyclic reduction (bsq_cr.cu)
+template <class T>
+struct CrPtrs {
+    const T *ax, *bx, *cx, *ay, *by, *cy;  // the operator's diagonals
+    const T *rx, *ry;                      // right-hand sides (ghosts folded in-kernel)
+    const T *gp, *gq;                      // ghost sources, as SolvePtrs
+    T *outx, *outy;
+    unsigned int *bad;                     // min error key (0xFFFFFFFF: none)
+    unsigned int key_base;                 // (solve phase - 1) << 31
+};
+
 template <class T>
 struct CorrectPtrs {
     const T *bu, *bv, *fs, *gs;     // quadrature bases and stored F*_n, G*_n
@@ -73,6 +84,9 @@ template <class T>
 void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, bool pos_pivots,
                   cudaStream_t st, int mode = SOLVE_FULL);
 int solve_chunk_elems(int elem_bytes);
+template <class T>
+void launch_cr(const Consts<T> &C, const CrPtrs<T> &K, cudaStream_t st);
+size_t cr_smem_bytes(int nx, int ny, int elem);
 template <class T>
 void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st);
 template <class T>

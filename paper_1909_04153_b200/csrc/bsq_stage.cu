@@ -351,16 +351,17 @@ void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A,
                   cudaStream_t st) {
     if constexpr (sizeof(T) == 8) {
         launch_stage_tiled(C, P, A, predict, st);
-        return;
+    } else {
+        const size_t smem = sizeof(StageSmem<T>);
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(k_stage<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            attr_set = true;
+        }
+        dim3 grid((C.L.nx + SW_ - 1) / SW_, (C.L.ny + STY - 1) / STY);
+        k_stage<T><<<grid, SW_ * SNW, smem, st>>>(C, P, A, predict);
     }
-    const size_t smem = sizeof(StageSmem<T>);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_stage<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
-    dim3 grid((C.L.nx + SW_ - 1) / SW_, (C.L.ny + STY - 1) / STY);
-    k_stage<T><<<grid, SW_ * SNW, smem, st>>>(C, P, A, predict);
 }
 
 template void launch_stage<double>(const Consts<double> &, const DevParams *,

@@ -186,8 +186,6 @@ class Simulator:
         self.phys = phys if phys is not None else PhysParams()
         if solver not in SOLVERS:
             raise ValueError(f"unknown solver {solver!r}; expected one of {SOLVERS}")
-        if solver != "thomas":
-            raise NotImplementedError("the B200 build implements the default Thomas solver")
         self.solver = solver
         self.h_dry = h_dry if h_dry is not None else 100.0 * bathy.h_eps
         if self.h_dry < 0.0:
@@ -205,7 +203,7 @@ class Simulator:
         d = nat.Desc()
         d.nx, d.ny = grid.nx, grid.ny
         d.precision = nat.FP64 if precision == "fp64" else nat.FP32
-        d.solver = nat.THOMAS
+        d.solver = nat.THOMAS if solver == "thomas" else nat.CR
         d.cross_correction = 1 if cross_correction else 0
         self._bands = [None] * 4
         for k, (side, pol, kind) in enumerate(zip(bc.SIDES, self._policies, self._kinds)):
@@ -375,6 +373,8 @@ class Simulator:
                                          f"(j={idx // nx}, i={idx % nx}) at t={t:.6g}")
         self.last_scheme = "euler" if euler else "ab3"
         if rc == nat.BSQ_ERR_SINGULAR:
+            if self.solver == "cr":  # which of _kernels.py:419-446 fired
+                raise ZeroDivisionError(nat.lib().bsq_last_error().decode(errors="replace"))
             raise ZeroDivisionError("singular tridiagonal system: zero pivot")
         g = self.bathy.grid
         if res.clamped > 0.0:

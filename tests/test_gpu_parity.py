@@ -40,7 +40,7 @@ def run_sim(sim, steps, err_type=stepper.InstabilityError):
     return np.array(recs, dtype=np.float64).reshape(-1, 6), abort
 
 
-@pytest.mark.parametrize("name", [n for n in gc.RUNS if n != "hump_cr"])
+@pytest.mark.parametrize("name", gc.RUNS)
 def test_golden_run_bitwise(name):
     z = gc.load(name)
     bathy, state, bounds, phys, ckw, skw = gc.inputs(z)
@@ -161,13 +161,13 @@ def test_ghost_fill_matches_oracle_policies(kinds):
         assert np.array_equal(getattr(got, f), getattr(ref_state, f)), f
 
 
-def _vs_oracle(case, steps, threads=8):
+def _vs_oracle(case, steps, threads=8, solver="thomas"):
     sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
                             stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
-                            h_dry=case.h_dry)
+                            h_dry=case.h_dry, solver=solver)
     ora = orc.OracleSimulator(case.bathy, case.state.copy(), case.boundaries,
                               orc.OController(dt_init=case.dt_init), phys=case.phys,
-                              h_dry=case.h_dry, threads=threads)
+                              h_dry=case.h_dry, threads=threads, solver=solver)
     for k in range(steps):
         a, b = sim.advance(), ora.advance()
         assert (a.dt, a.max_cfl, a.max_speed, a.max_depth) == \
@@ -184,6 +184,13 @@ def test_shoal_sponges_maker_256_vs_oracle_bitwise():
 
 def test_rip_irregular_friction_512_vs_oracle_bitwise():
     _vs_oracle(make_case("C4", scale=8), 40)
+
+
+def test_cyclic_reduction_solver_256_vs_oracle_bitwise():
+    """solver="cr" (cyclic_reduction_batch, _kernels.py:384-451), 256^2 with
+    sponges and a maker; non-power-of-two lines exercise the identity padding."""
+    _vs_oracle(make_case("C3", scale=4), 30, solver="cr")
+    _vs_oracle(make_case("C4", scale=12), 10, solver="cr")
 
 
 def test_rip_4096_full_size_vs_oracle_bitwise():
@@ -246,6 +253,28 @@ def test_singular_operator_raises_zero_division():
             phys=phys)
     with pytest.raises(ZeroDivisionError):
         sim.advance()
+
+
+def test_singular_operator_cr_reports_reduction():
+    """solver="cr" raises the reference's reduction-phase message
+    (_kernels.py:419), like the oracle on the same inputs."""
+    grid = Grid(8, 6, 1.0, 1.0)
+    from paper_1909_04153_b200.grid import build_bathymetry
+    bathy = build_bathymetry(grid, np.full((6, 8), -1.0), ws=0.0)
+    phys = PhysParams(b_disp=-0.8333333333333334)
+    walls = bc.Boundaries(west=bc.Wall(), east=bc.Wall(), south=bc.Wall(), north=bc.Wall())
+    mk = lambda: FieldState(np.maximum(0.0, bathy.bed_eff), np.zeros(grid.shape_padded),
+                            np.zeros(grid.shape_padded))
+    with pytest.warns(UserWarning):
+        sim = stepper.Simulator(bathy, mk(), walls, stepper.TimeController(dt_init=0.01),
+                                phys=phys, solver="cr")
+    ora = orc.OracleSimulator(bathy, mk(), walls, orc.OController(dt_init=0.01), phys=phys,
+                              solver="cr")
+    with pytest.raises(ZeroDivisionError) as want:
+        ora.advance()
+    with pytest.raises(ZeroDivisionError) as got:
+        sim.advance()
+    assert str(got.value) == str(want.value) == "singular tridiagonal system in reduction"
 
 
 def test_pending_rollback_keeps_committed_state():

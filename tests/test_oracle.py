@@ -98,3 +98,17 @@ def test_oracle_zero_pivot_raises():
     dd = np.array([[1.0, 0.0, 1.0]])
     with pytest.raises(ZeroDivisionError):
         orc.thomas_batch(dl, dd, np.zeros((1, 3)), np.ones((1, 3)))
+
+
+@pytest.mark.parametrize("dl,dd,du,msg", [
+    # messages as the reference's cyclic_reduction_batch raises them on these
+    # inputs (_kernels.py:419, :439; checked against the reference run here)
+    (np.zeros((2, 4)), np.array([[1.0, 1, 1, 1], [0.0, 1, 1, 1]]), np.zeros((2, 4)),
+     "singular tridiagonal system in reduction"),
+    (np.array([[0.0, 1.0]]), np.array([[1.0, 1.0]]), np.array([[1.0, 0.0]]),
+     "singular tridiagonal system: zero core determinant"),
+])
+def test_oracle_cr_singular_messages(dl, dd, du, msg):
+    with pytest.raises(ZeroDivisionError) as exc:
+        orc.cr_batch(dl, dd, du, np.ones(dd.shape))
+    assert str(exc.value) == msg
