@@ -55,7 +55,7 @@ def summary(rep: str, cells: int) -> str:
         if heavy is None or ms > heavy[1]:
             heavy = (d["Kernel Name"], ms)
     if heavy:
-        k = short(heavy[0]).split("<")[0]
+        k = short(heavy[0]).split("<")[0].split("::")[-1]
         sass = ncu_csv(["-i", rep, "--page", "source", "--csv", "-k", f"regex:{k}",
                         "--print-source", "sass"])
         h = sass[1]
