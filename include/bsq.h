@@ -177,6 +177,38 @@ int bsq_array_layout(bsq_ctx *ctx, int array, size_t *byte_offset, int *pitch, i
  * (a sharded run raises if any rank is singular) */
 int bsq_pivot_flags(bsq_ctx *ctx, int *all_positive, int *singular);
 
+/* -- per-step observers on device ----------------------------
+ * Replace the host observers of the reference run loop (cli.py:635-649),
+ * which read the whole host state after every step:
+ *   GaugeRecorder.record (scenario.py:184-202) reads w, P, Q at a few cells;
+ *   MaxSurfaceTracker.update (scenario.py:297-299) folds interior w into a
+ *   running np.maximum. */
+/* Gauge cells, padded (row, col) of this context's grid (gauge_cell,
+ * scenario.py:155-161); n = 0 clears.  Every step's k_final then samples
+ * them in its last CTA and they come back with the step result. */
+int bsq_set_gauges(bsq_ctx *ctx, const int *rows, const int *cols, int n);
+/* n x 3 doubles (w, P, Q) at the gauges, committed state */
+int bsq_gauge_values(bsq_ctx *ctx, double *out);
+/* Running max of interior w (padded-layout device buffer owned by the ctx):
+ *   BSQ_MAX_RESET  allocate if needed and fill with -inf
+ *   BSQ_MAX_FOLD   fold the committed state (np.maximum, NaN propagates);
+ *                  deferred: the next step's stage kernel does it in its
+ *                  pass over w, at no extra HBM pass
+ *   BSQ_MAX_FLUSH  run a pending fold now
+ *   BSQ_MAX_OFF    free */
+enum { BSQ_MAX_OFF = 0, BSQ_MAX_RESET = 1, BSQ_MAX_FOLD = 2, BSQ_MAX_FLUSH = 3 };
+int bsq_max_tracker(bsq_ctx *ctx, int op);
+/* ny x nx running max (flushes a pending fold first) */
+int bsq_download_max(bsq_ctx *ctx, double *out);
+
+/* -- artifact formatting (host only, no device needed) --------
+ * Append `nrows` rows of `ncols` doubles (row stride `stride` elements) to
+ * the file at `path` as the reference's ESRI-ASCII data block
+ * (grid.py:262-267: " ".join(f"{v:.17g}"), one line per row, the north row
+ * first when `north_first`).  Returns the bytes written, or -1. */
+long long bsq_append_rows(const char *path, const double *values, long nrows, long ncols,
+                          long stride, int north_first);
+
 /* -- timing support ------------------------------------------------------ */
 /* When enabled, bsq_step brackets each kernel with CUDA events on the
  * library stream; bsq_kernel_times returns the last step's per-kernel

@@ -19,6 +19,8 @@ FP64, FP32 = 0, 1
 THOMAS, CR = 0, 1
 
 _dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int)
+MAX_OFF, MAX_RESET, MAX_FOLD, MAX_FLUSH = range(4)
 
 
 class Desc(ctypes.Structure):
@@ -96,6 +98,12 @@ SIGNATURES = [
                                         ctypes.POINTER(ctypes.c_int)]),
     ("bsq_pivot_flags", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
                                        ctypes.POINTER(ctypes.c_int)]),
+    ("bsq_set_gauges", ctypes.c_int, [ctypes.c_void_p, _ip, _ip, ctypes.c_int]),
+    ("bsq_gauge_values", ctypes.c_int, [ctypes.c_void_p, _dp]),
+    ("bsq_max_tracker", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    ("bsq_download_max", ctypes.c_int, [ctypes.c_void_p, _dp]),
+    ("bsq_append_rows", ctypes.c_longlong, [ctypes.c_char_p, _dp, ctypes.c_long, ctypes.c_long,
+                                            ctypes.c_long, ctypes.c_int]),
 ]
 
 _lib = None
@@ -116,6 +124,10 @@ def lib():
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+def iptr(a):
+    return a.ctypes.data_as(_ip)
 
 
 def ptr(a):

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -181,6 +182,15 @@ struct Engine : EngineBase {
     const char *ev_name[kMaxEv] = {};
     int nev = 0, last_n = 0;
     float last_ms[kMaxEv] = {};
+    // observers: gauge cells gathered by k_final's last CTA,
+    // and the running max of w folded by the next stage kernel
+    long long *d_goff = nullptr;
+    T *d_gval = nullptr, *h_gstage = nullptr;  // device / pinned staging, ng x 3
+    std::vector<double> g_pend, g_com;  // samples of the pending / committed state
+    int ng = 0;
+    bool g_fresh = false;   // g_com holds the committed state's values
+    T *maxw = nullptr;      // padded layout, interior used
+    bool fold_req = false;  // fold the committed state into maxw at the next stage
     SolveMaps maps;                  // TMA descriptors (out slots patched per launch)
     CUtensorMap map_xout[3], map_yout[3];  // pending P/Q of state 0, state 1; P2/Q2
 
@@ -197,6 +207,10 @@ struct Engine : EngineBase {
         if (hres) cudaFreeHost(hres);
         if (hfac) cudaFreeHost(hfac);
         if (hstage) cudaFreeHost(hstage);
+        if (h_gstage) cudaFreeHost(h_gstage);
+        if (d_goff) cudaFree(d_goff);
+        if (d_gval) cudaFree(d_gval);
+        if (maxw) cudaFree(maxw);
         if (own_stream && st) cudaStreamDestroy(st);
     }
 
@@ -451,6 +465,7 @@ struct Engine : EngineBase {
             return rc;
         CU(cudaStreamSynchronize(st));
         pending = false;
+        g_fresh = false;
         return BSQ_OK;
     }
     int download_state(int which, double *w, double *p, double *q) {
@@ -537,6 +552,7 @@ struct Engine : EngineBase {
         A.us = arr[A_US];
         A.vs = arr[A_VS];
         A.bad = dres->stage_bad;
+        A.maxw = fold_req ? maxw : nullptr;
         return A;
     }
 
@@ -613,6 +629,7 @@ struct Engine : EngineBase {
         }
         case BSQ_PH_STAGE:
             launch_stage(C, dparams, stage_ptrs(slot), 1, st);
+            fold_req = false;
             ev_mark("stage");
             launch_ghost(C, dparams, 1, W(nxt), Pp(cur), Qq(cur), W(nxt), Pp(nxt), Qq(nxt), st);
             ev_mark("ghost_n");
@@ -680,11 +697,17 @@ struct Engine : EngineBase {
         F.part = part;
         F.counter = counter;
         F.res = dres;
+        F.goff = d_goff;
+        F.ng = ng;
+        F.gval = d_gval;
         launch_final(C, F, st);
         ev_mark("final");
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
+        if (ng)
+            CU(cudaMemcpyAsync(h_gstage, d_gval, sizeof(T) * 3 * ng, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
+        for (int k = 0; k < 3 * ng; k++) g_pend[k] = double(h_gstage[k]);
         if (timing) {
             last_n = nev - 1;
             for (int k = 1; k < nev; k++) cudaEventElapsedTime(&last_ms[k - 1], ev[k - 1], ev[k]);
@@ -758,6 +781,95 @@ struct Engine : EngineBase {
         head = pend_slot;
         if (nlev < 3) nlev++;
         pending = false;
+        g_com = g_pend;
+        g_fresh = ng > 0;
+        return BSQ_OK;
+    }
+
+    // -- observers ----------------------------------------------------------------------
+    int set_gauges(const int *rows, const int *cols, int n) {
+        if (n < 0 || (n > 0 && (!rows || !cols))) return fail(BSQ_ERR_BAD_ARG, "bad gauge list");
+        std::vector<long long> off(n);
+        for (int k = 0; k < n; k++) {
+            if (rows[k] < GL || rows[k] >= d.ny + GL || cols[k] < GL || cols[k] >= d.nx + GL)
+                return fail(BSQ_ERR_BAD_ARG, "gauge cell outside the interior");
+            off[k] = L.at(rows[k], cols[k]);
+        }
+        CU(cudaStreamSynchronize(st));
+        if (d_goff) cudaFree(d_goff);
+        if (d_gval) cudaFree(d_gval);
+        if (h_gstage) cudaFreeHost(h_gstage);
+        d_goff = nullptr;
+        d_gval = nullptr;
+        h_gstage = nullptr;
+        ng = n;
+        g_pend.assign(3 * (size_t)n, 0.0);
+        g_com.assign(3 * (size_t)n, 0.0);
+        g_fresh = false;
+        if (n == 0) return BSQ_OK;
+        CU(cudaMalloc(&d_goff, sizeof(long long) * n));
+        CU(cudaMalloc(&d_gval, sizeof(T) * 3 * n));
+        CU(cudaMallocHost(&h_gstage, sizeof(T) * 3 * n));
+        CU(cudaMemcpyAsync(d_goff, off.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+        return BSQ_OK;
+    }
+
+    // (w, P, Q) at every gauge cell of the committed state: the last step's
+    // k_final sample when it is current, else one gather launch
+    int gauge_values(double *out) {
+        if (!ng) return BSQ_OK;
+        if (!g_fresh) {
+            launch_gather(W(cur), Pp(cur), Qq(cur), d_goff, ng, d_gval, st);
+            CU(cudaGetLastError());
+            CU(cudaMemcpyAsync(h_gstage, d_gval, sizeof(T) * 3 * ng, cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            for (int k = 0; k < 3 * ng; k++) g_com[k] = double(h_gstage[k]);
+            g_fresh = true;
+        }
+        std::memcpy(out, g_com.data(), sizeof(double) * 3 * ng);
+        return BSQ_OK;
+    }
+
+    int max_tracker(int op) {
+        switch (op) {
+        case BSQ_MAX_OFF:
+            CU(cudaStreamSynchronize(st));
+            if (maxw) cudaFree(maxw);
+            maxw = nullptr;
+            fold_req = false;
+            return BSQ_OK;
+        case BSQ_MAX_RESET: {
+            if (!maxw) CU(cudaMalloc(&maxw, sizeof(T) * (size_t)L.elems()));
+            const T ninf = -std::numeric_limits<T>::infinity();
+            std::vector<T> h((size_t)L.elems(), ninf);
+            CU(cudaMemcpyAsync(maxw, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, st));
+            CU(cudaStreamSynchronize(st));
+            fold_req = false;
+            return BSQ_OK;
+        }
+        case BSQ_MAX_FOLD:
+            if (!maxw) return fail(BSQ_ERR_BAD_ARG, "max tracker not enabled");
+            fold_req = true;  // the next stage kernel folds the committed state
+            return BSQ_OK;
+        case BSQ_MAX_FLUSH:
+            if (!maxw) return fail(BSQ_ERR_BAD_ARG, "max tracker not enabled");
+            if (fold_req) {
+                launch_fold_max(C, W(cur), maxw, st);
+                CU(cudaGetLastError());
+                fold_req = false;
+            }
+            return BSQ_OK;
+        default:
+            return fail(BSQ_ERR_BAD_ARG, "unknown max-tracker op");
+        }
+    }
+
+    int download_max(double *out) {
+        if (!maxw) return fail(BSQ_ERR_BAD_ARG, "max tracker not enabled");
+        int rc;
+        if ((rc = max_tracker(BSQ_MAX_FLUSH)) || (rc = download_interior(out, maxw))) return rc;
+        CU(cudaStreamSynchronize(st));
         return BSQ_OK;
     }
 
@@ -766,6 +878,7 @@ struct Engine : EngineBase {
         CU(cudaMemsetAsync(dres, 0xFF, sizeof(DevResult), st));
         const int slot = (head + 1) % 4;
         launch_stage(C, dparams, stage_ptrs(slot), 0, st);
+        fold_req = false;
         CU(cudaGetLastError());
         int rc;
         for (int k = 0; k < 5; k++)
@@ -979,6 +1092,26 @@ int bsq_speed_extrema(bsq_ctx *c, double *out3) {
 int bsq_fill_ghosts(bsq_ctx *c, const double *eta, const double *flux) {
     if (!c || !eta || !flux) return fail(BSQ_ERR_BAD_ARG, "null argument");
     return ENGINE(c, e->fill_ghosts(eta, flux));
+}
+
+int bsq_set_gauges(bsq_ctx *c, const int *rows, const int *cols, int n) {
+    if (!c) return fail(BSQ_ERR_BAD_ARG, "null ctx");
+    return ENGINE(c, e->set_gauges(rows, cols, n));
+}
+
+int bsq_gauge_values(bsq_ctx *c, double *out) {
+    if (!c || !out) return fail(BSQ_ERR_BAD_ARG, "null argument");
+    return ENGINE(c, e->gauge_values(out));
+}
+
+int bsq_max_tracker(bsq_ctx *c, int op) {
+    if (!c) return fail(BSQ_ERR_BAD_ARG, "null ctx");
+    return ENGINE(c, e->max_tracker(op));
+}
+
+int bsq_download_max(bsq_ctx *c, double *out) {
+    if (!c || !out) return fail(BSQ_ERR_BAD_ARG, "null argument");
+    return ENGINE(c, e->download_max(out));
 }
 
 int bsq_set_timing(bsq_ctx *c, int enable) {

@@ -171,6 +171,14 @@ __global__ void __launch_bounds__(FT) k_final(Consts<T> C, FinalPtrs<T> F) {
         a.nan |= pp->dev_nan;
     }
     a = red_block(a);
+    // gauge cells of the new state (scenario.py:184-202 reads w, P, Q there);
+    // other CTAs wrote them: read through L2
+    for (int g = tid; g < F.ng; g += FT) {
+        const long long o = F.goff[g];
+        F.gval[3 * g] = __ldcg(F.w + o);
+        F.gval[3 * g + 1] = __ldcg(F.pout + o);
+        F.gval[3 * g + 2] = __ldcg(F.qout + o);
+    }
     if (tid == 0) {
         F.res->max_rate = a.rate;
         F.res->max_speed = a.speed;
@@ -204,6 +212,31 @@ __global__ void __launch_bounds__(FT) k_extrema(Consts<T> C, const T *w, const T
     }
 }
 
+// gauge gather outside a step (initial record, after a state upload)
+template <class T>
+__global__ void k_gather(const T *w, const T *p, const T *q, const long long *goff, int ng,
+                         T *gval) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ng) return;
+    const long long o = goff[g];
+    gval[3 * g] = w[o];
+    gval[3 * g + 1] = p[o];
+    gval[3 * g + 2] = q[o];
+}
+
+// MaxSurfaceTracker.update (scenario.py:297-299): np.maximum(max_w, w) over
+// the interior, numpy's NaN-propagating rule; the stage kernel folds the same
+// way when a fold is pending, this is the stand-alone flush
+template <class T>
+__global__ void k_fold_max(Consts<T> C, const T *w, T *maxw) {
+    const Layout L = C.L;
+    const int I = GL + blockIdx.x * blockDim.x + threadIdx.x;
+    const int J = GL + blockIdx.y;
+    if (I >= L.nx + GL) return;
+    const long o = L.at(J, I);
+    maxw[o] = np_maximum(maxw[o], w[o]);
+}
+
 static dim3 final_grid(int nx, int ny) { return dim3((nx + FX - 1) / FX, (ny + FY * FR - 1) / (FY * FR)); }
 
 int final_blocks(int nx, int ny) {
@@ -222,6 +255,24 @@ void launch_extrema(const Consts<T> &C, const T *w, const T *p, const T *q, cons
     k_extrema<T><<<final_grid(C.L.nx, C.L.ny), dim3(FX, FY), 0, st>>>(C, w, p, q, be, part);
 }
 
+template <class T>
+void launch_gather(const T *w, const T *p, const T *q, const long long *goff, int ng, T *gval,
+                   cudaStream_t st) {
+    if (ng > 0) k_gather<T><<<(ng + 127) / 128, 128, 0, st>>>(w, p, q, goff, ng, gval);
+}
+
+template <class T>
+void launch_fold_max(const Consts<T> &C, const T *w, T *maxw, cudaStream_t st) {
+    k_fold_max<T><<<dim3((C.L.nx + 255) / 256, C.L.ny), 256, 0, st>>>(C, w, maxw);
+}
+
+template void launch_gather<double>(const double *, const double *, const double *,
+                                    const long long *, int, double *, cudaStream_t);
+template void launch_gather<float>(const float *, const float *, const float *,
+                                   const long long *, int, float *, cudaStream_t);
+template void launch_fold_max<double>(const Consts<double> &, const double *, double *,
+                                      cudaStream_t);
+template void launch_fold_max<float>(const Consts<float> &, const float *, float *, cudaStream_t);
 template void launch_final<double>(const Consts<double> &, const FinalPtrs<double> &,
                                    cudaStream_t);
 template void launch_extrema<double>(const Consts<double> &, const double *, const double *,

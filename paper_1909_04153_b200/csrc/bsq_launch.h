@@ -17,6 +17,7 @@ struct StagePtrs {
     T *wn;                          // predicted w -> pending state's w
     T *bu, *bv, *us, *vs;           // quadrature bases and predicted U*, V*
     unsigned long long *bad;        // [5] first non-finite stage cell
+    T *maxw;                        // running max of w to fold this state into, or null
 };
 
 template <class T>
@@ -72,6 +73,9 @@ struct FinalPtrs {
     Partial *part;
     unsigned int *counter;
     DevResult *res;
+    const long long *goff;          // gauge cells (element offsets), gathered by the last CTA
+    int ng;
+    T *gval;                        // ng x (w, P, Q) of the new state
 };
 
 template <class T>
@@ -95,5 +99,11 @@ template <class T>
 void launch_extrema(const Consts<T> &C, const T *w, const T *p, const T *q, const T *be,
                     Partial *part, cudaStream_t st);
 int final_blocks(int nx, int ny);
+// observers: gauge gather and the running max of w
+template <class T>
+void launch_gather(const T *w, const T *p, const T *q, const long long *goff, int ng, T *gval,
+                   cudaStream_t st);
+template <class T>
+void launch_fold_max(const Consts<T> &C, const T *w, T *maxw, cudaStream_t st);
 
 }  // namespace bsq

@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
         cp_async_wait_all();  // this lane's cell inputs have landed
         if (cell) {
             const T wc = S.w[yy][x], pc = S.p[yy][x], qc = S.q[yy][x];
+            if (A.maxw) A.maxw[o] = np_maximum(A.maxw[o], wc);  // MaxSurfaceTracker fold
             const T c_be = ci[CI_BE][lane], c_d = ci[CI_D][lane];
             const T c_dx = ci[CI_DX][lane], c_dy = ci[CI_DY][lane];
             // fv_rates (_kernels.py:230-251)

@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(NT, 4) k_stage(Consts<T> C, const DevParams *_
     const int y = ty + 2, x = tx + 2;
     const long o = L.at(J, I);
     const T wc = S.w[y][x], pc = S.p[y][x], qc = S.q[y][x];
+    if (A.maxw) A.maxw[o] = np_maximum(A.maxw[o], wc);  // MaxSurfaceTracker fold
     const T be_ = S.bfx[ty][tx + 2], bw_ = S.bfx[ty][tx + 1];
     const T bn_ = S.bfy[ty + 2][tx], bs_ = S.bfy[ty + 1][tx];
 

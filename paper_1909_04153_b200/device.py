@@ -87,6 +87,30 @@ class DeviceStep:
                                                nat.ptr(p), nat.ptr(q)), "download_state")
         return w, p, q
 
+    # -- observers -------------------------------------------------
+    def set_gauges(self, cells):
+        """Padded (row, col) cells sampled by every step's k_final."""
+        rows = np.ascontiguousarray([c[0] for c in cells], dtype=np.int32)
+        cols = np.ascontiguousarray([c[1] for c in cells], dtype=np.int32)
+        nat.check(nat.lib().bsq_set_gauges(self._h, nat.iptr(rows), nat.iptr(cols), len(rows)),
+                  "set_gauges")
+        self._ngauge = len(rows)
+
+    def gauge_values(self) -> np.ndarray:
+        """(n, 3) w, P, Q at the gauges, committed state."""
+        out = np.empty((getattr(self, "_ngauge", 0), 3))
+        if out.shape[0]:
+            nat.check(nat.lib().bsq_gauge_values(self._h, nat.ptr(out)), "gauge_values")
+        return out
+
+    def max_tracker(self, op: int):
+        nat.check(nat.lib().bsq_max_tracker(self._h, op), "max_tracker")
+
+    def download_max(self) -> np.ndarray:
+        out = np.empty((self.ny, self.nx))
+        nat.check(nat.lib().bsq_download_max(self._h, nat.ptr(out)), "download_max")
+        return out
+
     def history(self, level: int, field: int) -> np.ndarray:
         out = np.empty((self.ny, self.nx))
         nat.check(nat.lib().bsq_download_history(self._h, level, field, nat.ptr(out)), "history")

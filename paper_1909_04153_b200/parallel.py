@@ -135,6 +135,14 @@ class LocalComm:
     def gather_state(self, locals_: dict, shape, ranges):
         return _assemble(locals_, shape, ranges)
 
+    def gather_values(self, per: dict, n: int):
+        """per[r] = (values (n, k), owned (n,) bool): the owners' rows."""
+        return _pick_owned(per.values(), n)
+
+    def gather_rows(self, per: dict, nx: int, ranges):
+        """per[r] = strip r's interior rows (n_r, nx) -> (ny, nx)."""
+        return np.concatenate([per[r] for r in range(self.world)], axis=0)
+
 
 class DistComm:
     """One strip per process; halos, boundary vectors and reductions over
@@ -254,6 +262,36 @@ class DistComm:
                for r in range(self.world)}
         return _assemble(per, shape, ranges)
 
+    def gather_values(self, per: dict, n: int):
+        (vals, owned), = per.values()
+        dev = self._dev()
+        v = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float64)).to(dev)
+        m = torch.from_numpy(np.ascontiguousarray(owned, dtype=np.int64)).to(dev)
+        vs = [torch.empty_like(v) for _ in range(self.world)]
+        ms = [torch.empty_like(m) for _ in range(self.world)]
+        self.dist.all_gather(vs, v, group=self.group)
+        self.dist.all_gather(ms, m, group=self.group)
+        return _pick_owned([(a.cpu().numpy(), b.cpu().numpy().astype(bool)) for a, b in zip(vs, ms)],
+                           n)
+
+    def gather_rows(self, per: dict, nx: int, ranges):
+        (mine,), dev = per.values(), self._dev()
+        n_max = max(n for _, n in ranges)
+        buf = torch.zeros((n_max, nx), dtype=torch.float64, device=dev)
+        buf[:mine.shape[0]] = torch.from_numpy(np.ascontiguousarray(mine)).to(dev)
+        bufs = [torch.empty_like(buf) for _ in range(self.world)]
+        self.dist.all_gather(bufs, buf, group=self.group)
+        return np.concatenate([b.cpu().numpy()[:ranges[r][1]] for r, b in enumerate(bufs)], axis=0)
+
+
+def _pick_owned(parts, n: int):
+    out = None
+    for vals, owned in parts:
+        if out is None:
+            out = np.zeros((n,) + vals.shape[1:])
+        out[owned] = vals[owned]
+    return out
+
 
 def _combine(parts: list, nx: int, rows0: list) -> dict:
     """Cross-strip reduction of per-strip step results, in rank order."""
@@ -362,6 +400,36 @@ class ShardedDevice:
             w, p, q = s.download()
             out[0][rows], out[1][rows], out[2][rows] = w, p, q
         return out
+
+    # -- observers: each strip samples the gauges in its rows -------------------
+    def set_gauges(self, cells):
+        self._gauges = [(int(j), int(i)) for j, i in cells]
+        self._gslots = {}
+        for r, s in self.strips.items():
+            row0, n = self.ranges[r]
+            mine = [k for k, (j, _) in enumerate(self._gauges) if row0 <= j - GHOST < row0 + n]
+            s.set_gauges([(self._gauges[k][0] - row0, self._gauges[k][1]) for k in mine])
+            self._gslots[r] = mine
+
+    def gauge_values(self) -> np.ndarray:
+        n = len(getattr(self, "_gauges", []))
+        per = {}
+        for r, s in self.strips.items():
+            vals, owned = np.zeros((n, 3)), np.zeros(n, dtype=bool)
+            mine = self._gslots[r]
+            if mine:
+                vals[mine] = s.gauge_values()
+                owned[mine] = True
+            per[r] = (vals, owned)
+        return self.comm.gather_values(per, n)
+
+    def max_tracker(self, op: int):
+        for s in self.strips.values():
+            s.max_tracker(op)
+
+    def download_max(self) -> np.ndarray:
+        per = {r: s.download_max() for r, s in self.strips.items()}
+        return self.comm.gather_rows(per, self.nx, self.ranges)
 
     def history(self, level: int, field: int) -> np.ndarray:
         out = np.empty((self.ny, self.nx))

@@ -327,6 +327,38 @@ class Simulator:
     def _pending_state(self) -> FieldState:
         return FieldState(*self._dev.download(pending=True))
 
+    # -- device observers (used by observers.py) -------------------
+    def watch_cells(self, cells) -> list[int]:
+        """Register padded (row, col) cells that every step samples on the
+        device; returns their slots in :meth:`cell_values`."""
+        if not hasattr(self, "_watch"):
+            self._watch, self._watch_slot = [], {}
+        slots, grew = [], False
+        for c in cells:
+            c = (int(c[0]), int(c[1]))
+            if c not in self._watch_slot:
+                self._watch_slot[c] = len(self._watch)
+                self._watch.append(c)
+                grew = True
+            slots.append(self._watch_slot[c])
+        if grew:
+            self._dev.set_gauges(self._watch)
+        return slots
+
+    def cell_values(self) -> np.ndarray:
+        """(n, 3) w, P, Q of the committed state at the watched cells."""
+        self._sync_host_edits()
+        return self._dev.gauge_values()
+
+    def max_tracker(self, op: int):
+        """Running max of interior w on the device (include/bsq.h BSQ_MAX_*)."""
+        self._sync_host_edits()
+        self._dev.max_tracker(op)
+
+    def download_max(self) -> np.ndarray:
+        self._sync_host_edits()
+        return self._dev.download_max()
+
     # -- single step ----------------------------------------------------------
     def advance(self, dt: float | None = None) -> StepRecord:
         c = self.controller

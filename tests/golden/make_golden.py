@@ -135,6 +135,26 @@ CASES = {
 }
 
 
+def case_island():
+    """Maker-driven waves around an emergent island: wet/dry gauges."""
+    grid = rg.Grid(40, 32, 0.25, 0.25)
+    xc, yc = np.meshgrid(grid.x_centers(), grid.y_centers())
+    bed = -0.6 + 0.9 * np.exp(-((xc - 6.0) ** 2 + (yc - 4.0) ** 2) / 1.5)
+    bathy = rg.build_bathymetry(grid, bed, ws=0.0)
+    d_west = float(bathy.depth[2:-2, 2].min())
+    b = rb.Boundaries(west=rb.SineMaker((rb.sine_component(0.02, 1.0, d_west),)),
+                      east=rb.Sponge(2.0, 8.0), south=rb.Wall(), north=rb.Wall())
+    return bathy, rg.still_state(bathy), b, rg.PhysParams(), dict(dt_init=0.01), {}, 250
+
+
+CASES["island"] = case_island
+
+# gauges of the observers fixture: (id, x, y, record_interval); g_dry sits on
+# the island (dry), g_shore at its edge, g_sponge inside the east sponge
+GAUGES = [("g_west", 1.1, 4.0, 0.0), ("g_shore", 5.0, 4.1, 0.05),
+          ("g_dry", 6.0, 4.0, 0.0), ("g_sponge", 9.4, 6.3, 0.2)]
+
+
 def encode_boundaries(b):
     kinds, comps, sponges = [], [], []
     for k, side in enumerate(SIDES):
@@ -231,6 +251,52 @@ def kernels_fixture():
     print("kernels fixture written")
 
 
+def observers_fixture():
+    """The reference run loop's observers (cli.py:621-647): a GaugeRecorder
+    and a MaxSurfaceTracker updated before the run and after every step, plus
+    the artifact bytes its writers produce (ASCII rasters, dt_history.csv,
+    gauge CSVs)."""
+    import io
+    import tempfile
+    from boussim import cli as rc
+    bathy, st, b, phys, ckw, skw, steps = case_island()
+    sim = stepper.Simulator(bathy, st, b, stepper.TimeController(**ckw), phys=phys, **skw)
+    specs = [rs.GaugeSpec(g, x, y, iv) for g, x, y, iv in GAUGES]
+    rec = rs.GaugeRecorder(bathy, specs)
+    tr = rs.MaxSurfaceTracker(bathy)
+    rec.record(sim.state, 0.0)
+    tr.update(sim.state)
+    for _ in range(steps):
+        r = sim.advance()
+        rec.record(sim.state, r.sim_time)
+        tr.update(sim.state)
+    out = {f"series_{g}": rec.series(g) for g, *_ in GAUGES}
+    out["cells"] = np.array([rs.gauge_cell(bathy.grid, x, y) for _, x, y, _ in GAUGES])
+    out["max_w"] = tr.max_w
+    tmp = tempfile.mkdtemp()
+    g = bathy.grid
+    rg.write_ascii_grid(os.path.join(tmp, "w.asc"), sim.state.w[2:-2, 2:-2], cellsize=g.dx,
+                        xll=g.x0, yll=g.y0)
+    rg.write_ascii_grid(os.path.join(tmp, "max_w.asc"), tr.max_w, cellsize=g.dx, xll=g.x0,
+                        yll=g.y0)
+    rc._write_dt_history(tmp, sim.records)
+    rec.write_csv(tmp)
+    for name in ["w.asc", "max_w.asc", "dt_history.csv"] + [f"gauge_{g}.csv" for g, *_ in GAUGES]:
+        with open(os.path.join(tmp, name), "rb") as fh:
+            out["file_" + name] = np.frombuffer(fh.read(), dtype=np.uint8)
+    # a raster of special values (formatting edge cases)
+    rng = np.random.default_rng(11)
+    v = rng.standard_normal((7, 9)) * 10.0 ** rng.integers(-320, 300, size=(7, 9))
+    v[0, :7] = [np.nan, -np.nan, np.inf, -np.inf, -0.0, 0.0, 5e-324]
+    v[1, :3] = [1e16, 123456.0, 0.1]
+    rg.write_ascii_grid(os.path.join(tmp, "special.asc"), v, 0.05, xll=-1.5, yll=2.0)
+    out["special"] = v
+    with open(os.path.join(tmp, "special.asc"), "rb") as fh:
+        out["file_special.asc"] = np.frombuffer(fh.read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "observers.npz"), **out)
+    print("observers fixture written", {k: v.shape for k, v in out.items() if k.startswith("series")})
+
+
 def weights_fixture():
     """ab3/increment weights for a spread of step triples (incl. clamped)."""
     from boussim import multistep as rm
@@ -254,3 +320,4 @@ if __name__ == "__main__":
         run_case(nm)
     kernels_fixture()
     weights_fixture()
+    observers_fixture()

@@ -13,7 +13,7 @@ from paper_1909_04153_b200.grid import Bathymetry, FieldState, Grid, PhysParams
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 SIDES = ("north", "south", "east", "west")
 RUNS = ["c1", "hump", "hump_cr", "maker_sponge", "rip_irregular", "runup", "dry_clamp",
-        "blowup", "fixed_single_pass", "lake"]
+        "blowup", "fixed_single_pass", "lake", "island"]
 
 
 def load(name):
