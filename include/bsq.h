@@ -209,6 +209,12 @@ int bsq_download_max(bsq_ctx *ctx, double *out);
 long long bsq_append_rows(const char *path, const double *values, long nrows, long ncols,
                           long stride, int north_first);
 
+/* Wavemaker forcing at time t (boundary.py:190-199): comps is
+ * n rows of (amplitude, omega, k, phase); out = (eta, normal flux), summed in
+ * component order with libm sin -- bitwise the reference's math.sin sums.
+ * Host only. */
+int bsq_maker_sums(const double *comps, int n, double t, double *out);
+
 /* -- timing support ------------------------------------------------------ */
 /* When enabled, bsq_step brackets each kernel with CUDA events on the
  * library stream; bsq_kernel_times returns the last step's per-kernel

@@ -69,3 +69,22 @@ extern "C" long long bsq_append_rows(const char *path, const double *values, lon
     if (std::fclose(f) != 0) return -1;
     return total;
 }
+
+// boundary.maker_surface_flux (reference boundary.py:190-199) for the
+// per-step host parameters: the same libm sin Python's math.sin calls, the
+// same operations in component order, so the sums are bitwise the
+// reference's (built with -ffp-contract=off).  comps is n x 4 rows of
+// (amplitude, omega, k, phase); out = (eta, flux).
+extern "C" int bsq_maker_sums(const double *comps, int n, double t, double *out) {
+    if ((!comps && n > 0) || n < 0 || !out) return BSQ_ERR_BAD_ARG;
+    double eta = 0.0, flux = 0.0;
+    for (int c = 0; c < n; c++) {
+        const double *r = comps + 4 * c;
+        const double s = r[0] * std::sin(r[1] * t + r[3]);
+        eta += s;
+        flux += s * (r[1] / r[2]);
+    }
+    out[0] = eta;
+    out[1] = flux;
+    return BSQ_OK;
+}

@@ -237,6 +237,23 @@ class Simulator:
         self._chain = controller.dt_init
         self._extrema = self._dev.speed_extrema()
         self._params = nat.StepParams()
+        # maker components as (amplitude, omega, k, phase) rows for the
+        # native per-step sums (bsq_maker_sums == boundary.maker_surface_flux)
+        self._maker_rows = [
+            np.ascontiguousarray([(c.amplitude, c.omega, c.k, c.phase) for c in pol.components],
+                                 dtype=np.float64).reshape(-1, 4)
+            if kind == "maker" else None
+            for pol, kind in zip(self._policies, self._kinds)]
+        self._maker_out = np.zeros(2)
+        self._maker_call = [
+            (nat.lib().bsq_maker_sums, nat.ptr(r), r.shape[0], nat.ptr(self._maker_out))
+            if r is not None else None for r in self._maker_rows]
+
+    def _maker(self, k: int, t: float):
+        fn, rows, n, out = self._maker_call[k]
+        fn(rows, n, t, out)
+        o = self._maker_out
+        return float(o[0]), float(o[1])
 
     def _make_device(self, desc, bathy, device):
         """The device engine for the whole grid (ShardedSimulator overrides)."""
@@ -382,9 +399,8 @@ class Simulator:
             pr.sc, pr.sp, pr.sp2 = s
         for k, (pol, kind) in enumerate(zip(self._policies, self._kinds)):
             if kind == "maker":
-                pr.maker_eta_t[k], pr.maker_flux_t[k] = bc.maker_surface_flux(pol.components, t)
-                pr.maker_eta_n[k], pr.maker_flux_n[k] = bc.maker_surface_flux(
-                    pol.components, t + dt_used)
+                pr.maker_eta_t[k], pr.maker_flux_t[k] = self._maker(k, t)
+                pr.maker_eta_n[k], pr.maker_flux_n[k] = self._maker(k, t + dt_used)
             band = self._bands[k]
             if band is not None:
                 fac = np.ascontiguousarray(bc.sponge_factors(band[0], band[1], band[2], dt_used))
