@@ -117,6 +117,19 @@ def test_maker_values_sum_in_order():
     assert flux == pytest.approx(s0 * (2.0 / 1.1) + s1 * (3.0 / 2.1), rel=1e-15)
 
 
+def test_native_maker_sums_bitwise():
+    """bsq_maker_sums (host C, libm sin) == boundary.maker_surface_flux, the
+    reference's math.sin loop, on the C4 JONSWAP spectrum (68 components)."""
+    from paper_1909_04153_b200.scenario import make_case
+    comps = make_case("C4", scale=16).boundaries.west.components
+    rows = np.ascontiguousarray([(c.amplitude, c.omega, c.k, c.phase) for c in comps])
+    out = np.zeros(2)
+    for t in np.concatenate([np.random.default_rng(5).uniform(0, 200, 3000),
+                             np.arange(0.0, 3.0, 0.00137)]):
+        assert nat.lib().bsq_maker_sums(nat.ptr(rows), len(comps), float(t), nat.ptr(out)) == 0
+        assert (out[0], out[1]) == bc.maker_surface_flux(comps, float(t))
+
+
 def test_product_fails_loudly_without_gpu():
     import torch
     if torch.cuda.is_available():
