@@ -11,7 +11,8 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libbsq.so")
+# BSQ_LIB: load another build of the library (A/B timing of variants only)
+LIB_PATH = os.environ.get("BSQ_LIB") or os.path.join(PKG, "lib", "libbsq.so")
 
 BSQ_OK, BSQ_ERR_BAD_ARG, BSQ_ERR_CUDA, BSQ_ERR_SINGULAR, BSQ_ERR_NO_DEVICE, BSQ_ERR_NCCL = range(6)
 WALL, MAKER, SPONGE = 0, 1, 2

@@ -67,31 +67,85 @@ __global__ void __launch_bounds__(NT, 4) k_stage(Consts<T> C, const DevParams *_
     const int I0 = GL + blockIdx.x * TX, J0 = GL + blockIdx.y * TY;
 
     // ---- A: tile + halo ------------------------------------------------------
-    for (int k = tid; k < HY * HX; k += NT) {
+    // Every global load of the phase is issued before the first shared store
+    // (fixed trip counts, unrolled), so the CTA pays one DRAM latency here
+    // instead of one per loop trip.
+    constexpr int PA = (HY * HX + NT - 1) / NT;
+    constexpr int PX = (TY * (TX + 3) + NT - 1) / NT;
+    constexpr int PY = ((TY + 3) * TX + NT - 1) / NT;
+    T lw[PA], lp[PA], lq[PA], lb[PA], ld[PA], lfx[PX], lfy[PY];
+#pragma unroll
+    for (int s = 0; s < PA; s++) {
+        const int k = tid + s * NT;
         const int y = k / HX, x = k - y * HX;
         const int J = J0 - 2 + y, I = I0 - 2 + x;
-        T w = 0, p = 0, q = 0, e = 0;
-        if (J < nyt && I < nxt) {
-            const long o = L.at(J, I);
-            w = A.w[o];
-            p = A.p[o];
-            q = A.q[o];
-            e = (w - A.be[o]) - A.dep[o];  // dispersion.py:87
-        }
-        S.w[y][x] = w;
-        S.p[y][x] = p;
-        S.q[y][x] = q;
-        S.eta[y][x] = e;
+        const bool in = k < HY * HX && J < nyt && I < nxt;
+        const long o = in ? L.at(J, I) : 0;
+        lw[s] = in ? A.w[o] : T(0);
+        lp[s] = in ? A.p[o] : T(0);
+        lq[s] = in ? A.q[o] : T(0);
+        lb[s] = in ? A.be[o] : T(0);
+        ld[s] = in ? A.dep[o] : T(0);
     }
-    for (int k = tid; k < TY * (TX + 3); k += NT) {
+#pragma unroll
+    for (int s = 0; s < PX; s++) {
+        const int k = tid + s * NT;
         const int y = k / (TX + 3), x = k - y * (TX + 3);
         const int J = J0 + y, I = I0 - 2 + x;
-        S.bfx[y][x] = (J < nyt && I <= nx + 2) ? A.bfx[L.at(J, I)] : T(0);
+        const bool in = k < TY * (TX + 3) && J < nyt && I <= nx + 2;
+        lfx[s] = in ? A.bfx[L.at(J, I)] : T(0);
     }
-    for (int k = tid; k < (TY + 3) * TX; k += NT) {
+#pragma unroll
+    for (int s = 0; s < PY; s++) {
+        const int k = tid + s * NT;
         const int y = k / TX, x = k - y * TX;
         const int J = J0 - 2 + y, I = I0 + x;
-        S.bfy[y][x] = (J <= ny + 2 && I < nxt) ? A.bfy[L.at(J, I)] : T(0);
+        const bool in = k < (TY + 3) * TX && J <= ny + 2 && I < nxt;
+        lfy[s] = in ? A.bfy[L.at(J, I)] : T(0);
+    }
+    // phase D's per-cell inputs that phase A does not read: start them towards
+    // L2 now (no registers held), so phase D's loads hit on chip
+    {
+        const int Jc = J0 + ty, Ic = I0 + tx;
+        if (Jc < ny + GL && Ic < nx + GL) {
+            const long oc = L.at(Jc, Ic);
+            prefetch_l2(A.ddx + oc);
+            prefetch_l2(A.ddy + oc);
+            if (predict && !P->euler) {
+#pragma unroll
+                for (int f = 0; f < 5; f++) {
+                    prefetch_l2(A.h1[f] + oc);
+                    prefetch_l2(A.h2[f] + oc);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < PA; s++) {
+        const int k = tid + s * NT;
+        if (k < HY * HX) {
+            const int y = k / HX, x = k - y * HX;
+            S.w[y][x] = lw[s];
+            S.p[y][x] = lp[s];
+            S.q[y][x] = lq[s];
+            S.eta[y][x] = (lw[s] - lb[s]) - ld[s];  // dispersion.py:87
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < PX; s++) {
+        const int k = tid + s * NT;
+        if (k < TY * (TX + 3)) {
+            const int y = k / (TX + 3), x = k - y * (TX + 3);
+            S.bfx[y][x] = lfx[s];
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < PY; s++) {
+        const int k = tid + s * NT;
+        if (k < (TY + 3) * TX) {
+            const int y = k / TX, x = k - y * TX;
+            S.bfy[y][x] = lfy[s];
+        }
     }
     __syncthreads();
 
@@ -239,11 +293,13 @@ __global__ void __launch_bounds__(NT, 4) k_stage(Consts<T> C, const DevParams *_
 
     // non-finite stage values (dispersion.py:92-98): first row-major cell
     const unsigned long long lin = (unsigned long long)(J - GL) * nx + (I - GL);
-    if (!isfinite(rw)) atomicMin(&A.bad[0], lin);
-    if (!isfinite(rp)) atomicMin(&A.bad[1], lin);
-    if (!isfinite(rq)) atomicMin(&A.bad[2], lin);
-    if (!isfinite(fs_)) atomicMin(&A.bad[3], lin);
-    if (!isfinite(gs_)) atomicMin(&A.bad[4], lin);
+    if (!(isfinite(rw) & isfinite(rp) & isfinite(rq) & isfinite(fs_) & isfinite(gs_))) {
+        if (!isfinite(rw)) atomicMin(&A.bad[0], lin);
+        if (!isfinite(rp)) atomicMin(&A.bad[1], lin);
+        if (!isfinite(rq)) atomicMin(&A.bad[2], lin);
+        if (!isfinite(fs_)) atomicMin(&A.bad[3], lin);
+        if (!isfinite(gs_)) atomicMin(&A.bad[4], lin);
+    }
 
     A.h0[0][o] = rw;
     A.h0[1][o] = rp;
