@@ -67,9 +67,9 @@ __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, 
     if (h < T(0)) h = T(0);
     const T hstar = h > C.h_eps ? h : C.h_eps;
     const T c = sqrt(C.g * h);
-    const T rh = rcp_rn(hstar);  // both quotients correctly rounded via one reciprocal
-    const T su = div_rcp(fabs(p), hstar, rh) + c;
-    const T sv = div_rcp(fabs(q), hstar, rh) + c;
+    const T nrh = -rcp_rn(hstar);  // both quotients correctly rounded via one reciprocal
+    const T su = div_nonneg(fabs(p), hstar, nrh) + c;
+    const T sv = div_nonneg(fabs(q), hstar, nrh) + c;
     const double rate = double(nb_max(su * C.inv_dx, sv * C.inv_dy));
     const double speed = double(nb_max(su, sv));
     if (rate > r.rate) r.rate = rate;
@@ -134,9 +134,11 @@ __global__ void __launch_bounds__(FT) k_final(Consts<T> C, FinalPtrs<T> F) {
         if (dv != dv) r.nan = 1;
         else if (double(dv) > r.dev) r.dev = double(dv);
         const unsigned long long lin = (unsigned long long)(J - GL) * nx + (I - GL);
-        if (!isfinite(w)) atomicMin(&F.res->state_bad[0], lin);
-        if (!isfinite(p)) atomicMin(&F.res->state_bad[1], lin);
-        if (!isfinite(q)) atomicMin(&F.res->state_bad[2], lin);
+        if (!(isfinite(w) & isfinite(p) & isfinite(q))) {
+            if (!isfinite(w)) atomicMin(&F.res->state_bad[0], lin);
+            if (!isfinite(p)) atomicMin(&F.res->state_bad[1], lin);
+            if (!isfinite(q)) atomicMin(&F.res->state_bad[2], lin);
+        }
         extrema_cell(C, w, p, q, be, r);
     }
     r = red_block(r);

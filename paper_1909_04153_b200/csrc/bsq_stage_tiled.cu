@@ -27,8 +27,15 @@
 
 namespace bsq {
 
+#ifndef BSQ_STAGE_MINB
+#define BSQ_STAGE_MINB 4  // CTAs per SM the register budget is sized for (64 regs)
+#endif
+
 namespace tiled {
-constexpr int TX = 32, TY = 8, NT = TX * TY;
+#ifndef BSQ_STAGE_TY
+#define BSQ_STAGE_TY 8
+#endif
+constexpr int TX = 32, TY = BSQ_STAGE_TY, NT = TX * TY;
 constexpr int HX = TX + 4, HY = TY + 4;       // tile + 2-cell halo
 constexpr int FXW = TX + 2, FYH = TY + 2;     // cells with x faces per row / rows with y faces
 constexpr int NXF = TY * FXW, NYF = FYH * TX; // face items
@@ -57,7 +64,7 @@ struct StageSmem {
 
 
 template <class T>
-__global__ void __launch_bounds__(NT, 4) k_stage(Consts<T> C, const DevParams *__restrict__ P,
+__global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const DevParams *__restrict__ P,
                                                  StagePtrs<T> A, int predict) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StageSmem<T> &S = *reinterpret_cast<StageSmem<T> *>(smem_raw);
@@ -107,7 +114,8 @@ __global__ void __launch_bounds__(NT, 4) k_stage(Consts<T> C, const DevParams *_
     // L2 now (no registers held), so phase D's loads hit on chip
     {
         const int Jc = J0 + ty, Ic = I0 + tx;
-        if (Jc < ny + GL && Ic < nx + GL) {
+        // one lane per 128-B line (16 doubles) issues the prefetch
+        if ((tx & (128 / sizeof(T) - 1)) == 0 && Jc < ny + GL && Ic < nx + GL) {
             const long oc = L.at(Jc, Ic);
             prefetch_l2(A.ddx + oc);
             prefetch_l2(A.ddy + oc);
