@@ -50,6 +50,16 @@ KERNEL_BYTES = {
 }
 
 
+def ncu_traffic():
+    """Per-kernel DRAM bytes per launch from the committed ncu --set full
+    capture (profiles/ncu_traffic.json, tools/ncu_summary.py --traffic-json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -306,8 +316,17 @@ def main():
     dom = max((k for k in avg if k in KERNEL_BYTES), key=lambda k: avg[k])
     achieved = KERNEL_BYTES[dom] * cells_gpu / (avg[dom] * 1e-3) / 1e9
     step_gbs = value / world * B_ALG_STEP
+    tr = ncu_traffic()
+    tk = (tr or {}).get("kernels", {}).get(dom) if args.scale == 1 else None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                "frac": achieved / hbm,
+                # DRAM bytes per launch of this kernel in the committed ncu capture
+                "traffic": tk["bytes_per_launch"] if tk else None,
+                "traffic_bytes_per_cell": tk["bytes_per_cell"] if tk else None,
+                "alg_bytes_per_launch": KERNEL_BYTES[dom] * cells_gpu,
+                "fp64_pipe_pct": tk.get("fp64_pipe_pct") if tk else None,
+                "traffic_source": tr.get("source") if tk else None,
+                "peak_kind": peak_kind,
                 "kernel_ms": avg, "step_achieved": step_gbs, "step_frac": step_gbs / hbm,
                 "step_bytes_per_cell": B_ALG_STEP}
 

@@ -104,12 +104,43 @@ def launches(path: str) -> str:
     return "\n".join(out)
 
 
+def traffic_json(rep: str, cells: int, source: str) -> dict:
+    """Per-kernel DRAM bytes per launch (first launch of each name) and the
+    fp64-pipe utilisation, for bench.py's roofline.traffic."""
+    rows = ncu_csv(["-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)])
+    hdr, units = rows[0], rows[1]
+    unit = dict(zip(hdr, units))["dram__bytes_read.sum"]
+    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(unit, 1e9)
+    names = {"k_stage": "stage", "k_correct": "correct", "k_final": "final"}
+    out, seen_solve = {}, 0
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        k = short(d["Kernel Name"]).split("<")[0].split("::")[-1]
+        if k == "k_solve_tma":
+            seen_solve += 1
+            key = f"solve{seen_solve}"
+        else:
+            key = names.get(k)
+        if not key or key in out:
+            continue
+        b = (float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * scale
+        out[key] = {"bytes_per_launch": b, "bytes_per_cell": b / cells,
+                    "ms": float(d["gpu__time_duration.sum"]),
+                    "fp64_pipe_pct": float(d["sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"])}
+    return {"source": source, "cells": cells, "kernels": out}
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("rep", nargs="?")
     ap.add_argument("--cells", type=int, default=4096 * 4096)
     ap.add_argument("--launches")
+    ap.add_argument("--traffic-json", help="write per-kernel DRAM bytes (for bench.py) here")
     a = ap.parse_args()
+    if a.traffic_json:
+        import json
+        with open(a.traffic_json, "w") as fh:
+            json.dump(traffic_json(a.rep, a.cells, a.rep), fh, indent=1)
     if a.launches:
         print(launches(a.launches))
     if a.rep:
