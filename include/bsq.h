@@ -48,6 +48,16 @@ enum { BSQ_SIDE_NORTH = 0, BSQ_SIDE_SOUTH = 1, BSQ_SIDE_EAST = 2, BSQ_SIDE_WEST 
 enum { BSQ_WALL = 0, BSQ_MAKER = 1, BSQ_SPONGE = 2 }; /* sponge ghosts mirror like a wall */
 enum { BSQ_FP64 = 0, BSQ_FP32 = 1 };
 enum { BSQ_THOMAS = 0, BSQ_CR = 1 };
+/* How a y-strip's column solves couple to the neighbouring strips:
+ *   BSQ_Y_PIPELINE  the global column's Thomas recurrence continues across
+ *                   ranks (dw / x boundary vectors, phases *F then *B): bitwise
+ *                   equal to one grid, but the sweeps serialize over ranks;
+ *   BSQ_Y_SPIKE     every strip factors and solves its block alone, then a
+ *                   partitioned (SPIKE) correction with precomputed spikes
+ *                   couples the blocks through a 2(G-1)-unknown system per
+ *                   column (bsq_spike_*): ranks run concurrently; equal to
+ *                   the one-grid solution to rounding (~1e-15 relative). */
+enum { BSQ_Y_PIPELINE = 0, BSQ_Y_SPIKE = 1 };
 
 /* Grid, physics and scheme constants.  Derived constants are passed in,
  * computed by the host exactly as the reference's Python computes them
@@ -69,6 +79,8 @@ typedef struct {
      * neighbour's interior rows, exchanged by the host between phases. */
     int32_t south_internal, north_internal;
     int32_t row0, ny_global;
+    int32_t y_coupling;        /* BSQ_Y_PIPELINE or BSQ_Y_SPIKE (strips only) */
+    int32_t pad_;
 } bsq_desc;
 
 /* Static fields (host pointers, reference layout; copied at create).  For a
@@ -169,13 +181,28 @@ int bsq_factor_tail(bsq_ctx *ctx, double *cw_north);
 enum {
     BSQ_ARR_W = 0, BSQ_ARR_P = 1, BSQ_ARR_Q = 2,                /* committed state */
     BSQ_ARR_W_NEW = 3, BSQ_ARR_P_NEW = 4, BSQ_ARR_Q_NEW = 5,    /* pending state */
-    BSQ_ARR_DW_IN = 6, BSQ_ARR_DW_OUT = 7, BSQ_ARR_X_IN = 8, BSQ_ARR_X_OUT = 9 /* nx vectors */
+    BSQ_ARR_DW_IN = 6, BSQ_ARR_DW_OUT = 7, BSQ_ARR_X_IN = 8, BSQ_ARR_X_OUT = 9, /* nx vectors */
+    BSQ_ARR_Q2 = 10                                             /* second-solve Q */
 };
 int bsq_array_layout(bsq_ctx *ctx, int array, size_t *byte_offset, int *pitch, int *xo,
                      int *elem_bytes);
 /* whether every Thomas pivot of this context is > 0, and whether one is 0
  * (a sharded run raises if any rank is singular) */
 int bsq_pivot_flags(bsq_ctx *ctx, int *all_positive, int *singular);
+
+/* -- y-strips with BSQ_Y_SPIKE --------------------------------------------
+ * Setup: every rank's 4 x nx spike boundary coefficients (bsq_spike_coeffs:
+ * v[first], v[last], w[first], w[last] per column, where v / w solve the
+ * strip's block against its south / north coupling column) are gathered into
+ * a G x 4 x nx table, in rank order, and given to every rank.
+ * Per solve (after BSQ_PH_SOLVE1F or BSQ_PH_SOLVE2F): gather every rank's
+ * first and last solved row of Q (BSQ_ARR_Q_NEW for solve 1, BSQ_ARR_Q2 for
+ * solve 2) into a device array G x 2 x nx of the context's precision, then
+ * bsq_spike_fix(solve, ...) solves the coupling system per column and
+ * corrects this strip's Q in place, on the library stream. */
+int bsq_spike_coeffs(bsq_ctx *ctx, double *out);
+int bsq_set_spike_table(bsq_ctx *ctx, const double *table, int nranks, int rank);
+int bsq_spike_fix(bsq_ctx *ctx, int solve, const void *ybound_device);
 
 /* -- per-step observers on device ----------------------------
  * Replace the host observers of the reference run loop (cli.py:635-649),

@@ -18,6 +18,7 @@ BSQ_OK, BSQ_ERR_BAD_ARG, BSQ_ERR_CUDA, BSQ_ERR_SINGULAR, BSQ_ERR_NO_DEVICE, BSQ_
 WALL, MAKER, SPONGE = 0, 1, 2
 FP64, FP32 = 0, 1
 THOMAS, CR = 0, 1
+Y_PIPELINE, Y_SPIKE = 0, 1
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)
@@ -35,7 +36,8 @@ class Desc(ctypes.Structure):
                 ("c_f", ctypes.c_double), ("theta", ctypes.c_double), ("h_eps", ctypes.c_double),
                 ("h_dry", ctypes.c_double), ("ws", ctypes.c_double),
                 ("south_internal", ctypes.c_int32), ("north_internal", ctypes.c_int32),
-                ("row0", ctypes.c_int32), ("ny_global", ctypes.c_int32)]
+                ("row0", ctypes.c_int32), ("ny_global", ctypes.c_int32),
+                ("y_coupling", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 class Static(ctypes.Structure):
@@ -45,6 +47,7 @@ class Static(ctypes.Structure):
 
 # phased step (y-strip sharding) and device array ids -- include/bsq.h
 PH_GHOST, PH_STAGE, PH_SOLVE1F, PH_SOLVE1B, PH_CORRECT, PH_SOLVE2F, PH_SOLVE2B, PH_FINAL = range(8)
+ARR_Q2 = 10
 ARR_W, ARR_P, ARR_Q, ARR_W_NEW, ARR_P_NEW, ARR_Q_NEW, ARR_DW_IN, ARR_DW_OUT, ARR_X_IN, ARR_X_OUT = \
     range(10)
 
@@ -99,6 +102,9 @@ SIGNATURES = [
                                         ctypes.POINTER(ctypes.c_int)]),
     ("bsq_pivot_flags", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int),
                                        ctypes.POINTER(ctypes.c_int)]),
+    ("bsq_spike_coeffs", ctypes.c_int, [ctypes.c_void_p, _dp]),
+    ("bsq_set_spike_table", ctypes.c_int, [ctypes.c_void_p, _dp, ctypes.c_int, ctypes.c_int]),
+    ("bsq_spike_fix", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     ("bsq_set_gauges", ctypes.c_int, [ctypes.c_void_p, _ip, _ip, ctypes.c_int]),
     ("bsq_gauge_values", ctypes.c_int, [ctypes.c_void_p, _dp]),
     ("bsq_max_tracker", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),

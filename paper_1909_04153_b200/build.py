@@ -20,7 +20,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(OUT_DIR, "libbsq.so")
-SOURCES = ["bsq_ghost.cu", "bsq_stage.cu", "bsq_stage_tiled.cu", "bsq_solve.cu", "bsq_cr.cu", "bsq_correct.cu",
+SOURCES = ["bsq_ghost.cu", "bsq_stage.cu", "bsq_stage_tiled.cu", "bsq_solve.cu", "bsq_cr.cu", "bsq_spike.cu", "bsq_correct.cu",
            "bsq_final.cu",
            "bsq_api.cu", "bsq_io.cpp"]
 HEADERS = ["bsq_device.cuh", "bsq_launch.h", "bsq_tma.cuh"]

@@ -47,12 +47,24 @@ enum Arr {
     A_AX, A_DENX, A_RDENX, A_CWX, A_AY, A_DENY, A_RDENY, A_CWY,
     A_BU, A_BV, A_US, A_VS, A_P2, A_Q2,
     A_BX, A_CX, A_BY, A_CY,  // diagonals for solver="cr"
+    A_SPV, A_SPW,            // BSQ_Y_SPIKE: south / north coupling spikes
     A_HIST0,  // 4 slots x 5 fields follow
     A_COUNT = A_HIST0 + 20
 };
 
 enum Small { S_CXL, S_CYL, S_FAC, S_PAR, S_RES, S_PART, S_CNT, S_DWIN, S_DWOUT, S_XIN, S_XOUT,
-             S_COUNT };
+             S_SPBT, S_COUNT };
+
+bool spike_mode(const bsq_desc *d) {
+    return d->y_coupling == BSQ_Y_SPIKE && (d->south_internal || d->north_internal);
+}
+
+// arrays a context does not use take no memory
+bool array_used(const bsq_desc *d, int k) {
+    if (k >= A_BX && k <= A_CY) return d->solver == BSQ_CR;
+    if (k == A_SPV || k == A_SPW) return spike_mode(d);
+    return true;
+}
 
 template <class T>
 Layout make_layout(const bsq_desc *d) {
@@ -73,7 +85,10 @@ size_t layout_bytes(const bsq_desc *d, size_t offs[A_COUNT + S_COUNT], int *fac_
     const Layout L = make_layout<T>(d);
     size_t off = 0;
     const size_t one = align256((size_t)L.elems() * sizeof(T));
-    for (int k = 0; k < A_COUNT; k++, off += one) offs[k] = off;
+    for (int k = 0; k < A_COUNT; k++) {
+        offs[k] = off;
+        if (array_used(d, k)) off += one;
+    }
     int fs = d->nx > d->ny ? d->nx : d->ny;
     fs = (fs + 31) / 32 * 32;
     *fac_stride = fs;
@@ -81,7 +96,7 @@ size_t layout_bytes(const bsq_desc *d, size_t offs[A_COUNT + S_COUNT], int *fac_
                                    sizeof(DevParams), sizeof(DevResult),
                                    sizeof(Partial) * (size_t)final_blocks(d->nx, d->ny), 256,
                                    sizeof(T) * d->nx, sizeof(T) * d->nx, sizeof(T) * d->nx,
-                                   sizeof(T) * d->nx};
+                                   sizeof(T) * d->nx, sizeof(T) * 2 * d->nx};
     for (int k = 0; k < S_COUNT; k++) {
         offs[A_COUNT + k] = off;
         off += align256(small[k]);
@@ -105,6 +120,8 @@ int check_desc(const bsq_desc *d) {
                                          "4096 (fp64) / 8192 (fp32) cells");
     }
     if (!(d->dx > 0 && d->dy > 0)) return fail(BSQ_ERR_BAD_ARG, "cell sizes must be positive");
+    if (d->y_coupling != BSQ_Y_PIPELINE && d->y_coupling != BSQ_Y_SPIKE)
+        return fail(BSQ_ERR_BAD_ARG, "y_coupling must be BSQ_Y_PIPELINE or BSQ_Y_SPIKE");
     if (d->south_internal || d->north_internal) {
         if (d->row0 < 0 || d->row0 + d->ny > d->ny_global)
             return fail(BSQ_ERR_BAD_ARG, "strip rows outside the global grid");
@@ -211,6 +228,7 @@ struct Engine : EngineBase {
         if (d_goff) cudaFree(d_goff);
         if (d_gval) cudaFree(d_gval);
         if (maxw) cudaFree(maxw);
+        if (d_sptab) cudaFree(d_sptab);
         if (own_stream && st) cudaStreamDestroy(st);
     }
 
@@ -336,11 +354,12 @@ struct Engine : EngineBase {
         }
         // y columns; a strip with an internal south side continues the global
         // column's recurrence from the south strip's last cw
-        if (d.south_internal && !f->cw_south)
+        const bool spike = spike_mode(&d);
+        if (d.south_internal && !spike && !f->cw_south)
             return fail(BSQ_ERR_BAD_ARG, "strip with an internal south side needs cw_south");
         cw_tail.assign(nx, 0.0);
         for (int i = 0; i < nx; i++) {
-            const bool cont = d.south_internal != 0;
+            const bool cont = d.south_internal != 0 && !spike;  // spike: each block alone
             double cw_prev = cont ? f->cw_south[i] : 0.0;
             for (int j = 0; j < ny; j++) {
                 const long h = (long)(j + GL) * nxt + i + GL;
@@ -358,6 +377,7 @@ struct Engine : EngineBase {
         }
         singular = sing;
         pos_pivots = pos;
+        if (spike) make_spikes(ay, deny, cwy, cyl);
         const size_t B = sizeof(T) * E;
         const std::vector<T> *src[12] = {&ax, &denx, &rdenx, &cwx, &ay, &deny, &rdeny, &cwy,
                                          &bxv, &cxv, &byv, &cyv};
@@ -368,6 +388,75 @@ struct Engine : EngineBase {
         CU(cudaMemcpyAsync(cx_last, cxl.data(), sizeof(T) * ny, cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(cy_last, cyl.data(), sizeof(T) * nx, cudaMemcpyHostToDevice, st));
         CU(cudaStreamSynchronize(st));  // host vectors go out of scope
+        return BSQ_OK;
+    }
+
+    // BSQ_Y_SPIKE: v = A^-1 (a_first e_first), w = A^-1 (c_last e_last) for
+    // every column of this strip's block, with the block's own LU factors
+    // (thomas_batch's recurrence on a unit right-hand side)
+    std::vector<double> sp_coef;  // 4 x nx: v_first, v_last, w_first, w_last
+    void make_spikes(const std::vector<T> &ay, const std::vector<T> &deny,
+                     const std::vector<T> &cwy, const std::vector<T> &cyl) {
+        const int nx = d.nx, ny = d.ny;
+        const long E = L.elems();
+        std::vector<T> vv(E, T(0)), ww(E, T(0));
+        std::vector<double> col(ny);
+        sp_coef.assign(4 * (size_t)nx, 0.0);
+        for (int i = 0; i < nx; i++) {
+            auto at = [&](int j) { return L.at(j + GL, i + GL); };
+            if (d.south_internal) {
+                double dw = double(ay[at(0)]) / double(deny[at(0)]);
+                col[0] = dw;
+                for (int j = 1; j < ny; j++) {
+                    dw = (0.0 - double(ay[at(j)]) * dw) / double(deny[at(j)]);
+                    col[j] = dw;
+                }
+                for (int j = ny - 2; j >= 0; j--) col[j] = col[j] - double(cwy[at(j)]) * col[j + 1];
+                for (int j = 0; j < ny; j++) vv[at(j)] = T(col[j]);
+                sp_coef[0 * (size_t)nx + i] = double(T(col[0]));
+                sp_coef[1 * (size_t)nx + i] = double(T(col[ny - 1]));
+            }
+            if (d.north_internal) {
+                col[ny - 1] = double(cyl[i]) / double(deny[at(ny - 1)]);
+                for (int j = ny - 2; j >= 0; j--) col[j] = 0.0 - double(cwy[at(j)]) * col[j + 1];
+                for (int j = 0; j < ny; j++) ww[at(j)] = T(col[j]);
+                sp_coef[2 * (size_t)nx + i] = double(T(col[0]));
+                sp_coef[3 * (size_t)nx + i] = double(T(col[ny - 1]));
+            }
+        }
+        cudaMemcpyAsync(arr[A_SPV], vv.data(), sizeof(T) * E, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(arr[A_SPW], ww.data(), sizeof(T) * E, cudaMemcpyHostToDevice, st);
+        cudaStreamSynchronize(st);
+    }
+
+    double *d_sptab = nullptr;  // G x 4 x nx, all ranks' spike coefficients
+    int sp_G = 0, sp_rank = 0;
+
+    int set_spike_table(const double *table, int G, int rank) {
+        if (!spike_mode(&d)) return fail(BSQ_ERR_BAD_ARG, "context is not a spike-coupled strip");
+        if (!table || G < 2 || G > 64 || rank < 0 || rank >= G)
+            return fail(BSQ_ERR_BAD_ARG, "bad spike table (2 <= ranks <= 64)");
+        if ((rank > 0) != (d.south_internal != 0) || (rank < G - 1) != (d.north_internal != 0))
+            return fail(BSQ_ERR_BAD_ARG, "rank does not match the strip's internal sides");
+        if (d_sptab) cudaFree(d_sptab);
+        d_sptab = nullptr;
+        CU(cudaMalloc(&d_sptab, sizeof(double) * 4 * (size_t)G * d.nx));
+        CU(cudaMemcpyAsync(d_sptab, table, sizeof(double) * 4 * (size_t)G * d.nx,
+                           cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+        sp_G = G;
+        sp_rank = rank;
+        return BSQ_OK;
+    }
+
+    int spike_fix(int solve, const void *ybound) {
+        if (!d_sptab) return fail(BSQ_ERR_BAD_ARG, "spike table not set");
+        if ((solve != 1 && solve != 2) || !ybound) return fail(BSQ_ERR_BAD_ARG, "bad spike_fix args");
+        T *x = solve == 1 ? Qq(1 - cur) : arr[A_Q2];
+        T *bt = (T *)(base + offs[A_COUNT + S_SPBT]);
+        launch_spike(C, sp_G, sp_rank, d_sptab, (const T *)ybound, bt, x, arr[A_SPV], arr[A_SPW],
+                     d.south_internal, d.north_internal, st);
+        CU(cudaGetLastError());
         return BSQ_OK;
     }
 
@@ -615,7 +704,8 @@ struct Engine : EngineBase {
     int phase(int ph, const bsq_step_params *p, bsq_step_result *r) {
         const int nxt = 1 - cur;
         const int slot = (head + 1) % 4;
-        const int fwd_mode = strip() ? SOLVE_X_YFWD : SOLVE_FULL;
+        const bool piped = strip() && !spike_mode(&d);  // rank-pipelined y recurrence
+        const int fwd_mode = piped ? SOLVE_X_YFWD : SOLVE_FULL;
         switch (ph) {
         case BSQ_PH_GHOST: {
             int rc = stage_params(p);
@@ -642,7 +732,7 @@ struct Engine : EngineBase {
             ev_mark("solve1");
             break;
         case BSQ_PH_SOLVE1B:
-            if (strip()) {
+            if (piped) {
                 launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st, SOLVE_YBWD);
                 ev_mark("solve1b");
             }
@@ -663,7 +753,7 @@ struct Engine : EngineBase {
             }
             break;
         case BSQ_PH_SOLVE2B:
-            if (d.cross_correction && strip()) {
+            if (d.cross_correction && piped) {
                 launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st, SOLVE_YBWD);
                 ev_mark("solve2b");
             }
@@ -766,6 +856,7 @@ struct Engine : EngineBase {
         case BSQ_ARR_DW_OUT: ptr = dw_out; break;
         case BSQ_ARR_X_IN: ptr = x_in; break;
         case BSQ_ARR_X_OUT: ptr = x_out; break;
+        case BSQ_ARR_Q2: ptr = arr[A_Q2]; break;
         default: return fail(BSQ_ERR_BAD_ARG, "unknown array id");
         }
         *off = (size_t)((const char *)ptr - base);
@@ -1092,6 +1183,25 @@ int bsq_speed_extrema(bsq_ctx *c, double *out3) {
 int bsq_fill_ghosts(bsq_ctx *c, const double *eta, const double *flux) {
     if (!c || !eta || !flux) return fail(BSQ_ERR_BAD_ARG, "null argument");
     return ENGINE(c, e->fill_ghosts(eta, flux));
+}
+
+int bsq_spike_coeffs(bsq_ctx *c, double *out) {
+    if (!c || !out) return fail(BSQ_ERR_BAD_ARG, "null argument");
+    return ENGINE(c, ([&] {
+        if (!spike_mode(&e->d)) return fail(BSQ_ERR_BAD_ARG, "context is not a spike-coupled strip");
+        std::memcpy(out, e->sp_coef.data(), sizeof(double) * e->sp_coef.size());
+        return (int)BSQ_OK;
+    })());
+}
+
+int bsq_set_spike_table(bsq_ctx *c, const double *table, int nranks, int rank) {
+    if (!c) return fail(BSQ_ERR_BAD_ARG, "null ctx");
+    return ENGINE(c, e->set_spike_table(table, nranks, rank));
+}
+
+int bsq_spike_fix(bsq_ctx *c, int solve, const void *ybound) {
+    if (!c) return fail(BSQ_ERR_BAD_ARG, "null ctx");
+    return ENGINE(c, e->spike_fix(solve, ybound));
 }
 
 int bsq_set_gauges(bsq_ctx *c, const int *rows, const int *cols, int n) {

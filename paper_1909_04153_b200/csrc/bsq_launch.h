@@ -99,6 +99,10 @@ template <class T>
 void launch_extrema(const Consts<T> &C, const T *w, const T *p, const T *q, const T *be,
                     Partial *part, cudaStream_t st);
 int final_blocks(int nx, int ny);
+// BSQ_Y_SPIKE: per-column coupling system + in-place correction of a strip's Q
+template <class T>
+void launch_spike(const Consts<T> &C, int G, int rank, const double *table, const T *yb, T *bt,
+                  T *x, const T *v, const T *w, int south, int north, cudaStream_t st);
 // observers: gauge gather and the running max of w
 template <class T>
 void launch_gather(const T *w, const T *p, const T *q, const long long *goff, int ng, T *gval,

@@ -87,6 +87,25 @@ class DeviceStep:
                                                nat.ptr(p), nat.ptr(q)), "download_state")
         return w, p, q
 
+    # -- BSQ_Y_SPIKE strips ---------------------------------------------------------
+    def spike_coeffs(self) -> np.ndarray:
+        """(4, nx): v_first, v_last, w_first, w_last of this strip's spikes."""
+        out = np.empty((4, self.nx))
+        nat.check(nat.lib().bsq_spike_coeffs(self._h, nat.ptr(out)), "spike_coeffs")
+        return out
+
+    def set_spike_table(self, table: np.ndarray, rank: int):
+        t = _f64(table)
+        nat.check(nat.lib().bsq_set_spike_table(self._h, nat.ptr(t), t.shape[0], rank),
+                  "set_spike_table")
+
+    def spike_fix(self, solve: int, ybound: torch.Tensor):
+        """Couple this strip's solve ``solve`` (1 or 2) to the others; ybound
+        is the (G, 2, nx) device tensor of every strip's first / last row."""
+        self._keep_yb = ybound  # alive until the stream has consumed it
+        nat.check(nat.lib().bsq_spike_fix(self._h, solve, ctypes.c_void_p(ybound.data_ptr())),
+                  "spike_fix")
+
     # -- observers (SURVEY 8 f1) -------------------------------------------------
     def set_gauges(self, cells):
         """Padded (row, col) cells sampled by every step's k_final."""

@@ -139,6 +139,19 @@ class LocalComm:
         """per[r] = (values (n, k), owned (n,) bool): the owners' rows."""
         return _pick_owned(per.values(), n)
 
+    # BSQ_Y_SPIKE: static spike coefficients once, solve boundary rows per solve
+    def gather_spike_table(self, per: dict, nx: int) -> np.ndarray:
+        return np.stack([per[r] for r in range(self.world)])
+
+    def spike_bounds(self, strips, arr: int, stream) -> dict:
+        with torch.cuda.stream(stream):
+            parts = []
+            for r in range(self.world):
+                R, n = strips[r].rows(arr), strips[r].ny
+                parts.append(torch.stack([R[GHOST, GHOST:-GHOST], R[GHOST + n - 1, GHOST:-GHOST]]))
+            yb = torch.stack(parts).contiguous()
+        return {r: yb for r in range(self.world)}
+
     def gather_rows(self, per: dict, nx: int, ranges):
         """per[r] = strip r's interior rows (n_r, nx) -> (ny, nx)."""
         return np.concatenate([per[r] for r in range(self.world)], axis=0)
@@ -283,6 +296,23 @@ class DistComm:
         self.dist.all_gather(bufs, buf, group=self.group)
         return np.concatenate([b.cpu().numpy()[:ranges[r][1]] for r, b in enumerate(bufs)], axis=0)
 
+    def gather_spike_table(self, per: dict, nx: int) -> np.ndarray:
+        (mine,) = per.values()
+        t = torch.from_numpy(np.ascontiguousarray(mine)).to(self._dev())
+        bufs = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(bufs, t, group=self.group)
+        return np.stack([b.cpu().numpy() for b in bufs])
+
+    def spike_bounds(self, strips, arr: int, stream) -> dict:
+        s = strips[self.rank]
+        with torch.cuda.stream(stream):
+            R, n = s.rows(arr), s.ny
+            mine = torch.stack([R[GHOST, GHOST:-GHOST], R[GHOST + n - 1, GHOST:-GHOST]]).contiguous()
+            bufs = [torch.empty_like(mine) for _ in range(self.world)]
+            self.dist.all_gather(bufs, mine, group=self.group)
+            yb = torch.stack(bufs).contiguous()
+        return {self.rank: yb}
+
 
 def _pick_owned(parts, n: int):
     out = None
@@ -337,8 +367,12 @@ def _assemble(per: dict, shape, ranges):
 class ShardedDevice:
     """Drop-in for DeviceStep over y-strips (the Simulator drives it)."""
 
-    def __init__(self, sim: "ShardedSimulator", desc, bathy, device, world: int, comm):
+    def __init__(self, sim: "ShardedSimulator", desc, bathy, device, world: int, comm,
+                 coupling: str = "pipeline"):
+        if coupling not in ("pipeline", "spike"):
+            raise ValueError(f"coupling must be 'pipeline' or 'spike', got {coupling!r}")
         self.sim, self.comm, self.world = sim, comm, world
+        self.spike = coupling == "spike" and world > 1
         self.nx, self.ny = desc.nx, desc.ny
         self.shape = (desc.ny + 2 * GHOST, desc.nx + 2 * GHOST)
         self.ranges = split_rows(desc.ny, world)
@@ -362,15 +396,25 @@ class ShardedDevice:
             d.ny, d.row0, d.ny_global = n, row0, desc.ny
             d.south_internal = 1 if r > 0 else 0
             d.north_internal = 1 if r < world - 1 else 0
+            d.y_coupling = nat.Y_SPIKE if self.spike else nat.Y_PIPELINE
             for s, (lo, ln, _) in zip((_N, _S), bands):
                 d.sponge_lo[s], d.sponge_len[s] = lo, ln
-            cws = comm.get_tail(tails, r, desc.nx) if r > 0 else None
+            # the pipelined recurrence continues the south strip's factorization;
+            # spike blocks are factored alone
+            cws = comm.get_tail(tails, r, desc.nx) if r > 0 and not self.spike else None
             strip = DeviceStep(d, _StripStatic(bathy, row0, n), device=dev, stream=self.stream,
                                cw_south=cws)
             self.strips[r] = strip
-            comm.pass_tail(tails, r, strip.factor_tail())
+            if not self.spike:
+                comm.pass_tail(tails, r, strip.factor_tail())
             sing.append(strip.pivot_flags()[1])
         self.singular = comm.any_flag(sing)
+        self.cross = bool(desc.cross_correction)
+        if self.spike:
+            table = comm.gather_spike_table({r: s.spike_coeffs() for r, s in self.strips.items()},
+                                            desc.nx)
+            for r, s in self.strips.items():
+                s.set_spike_table(table, r)
         first = self.strips[min(self.strips)]
         self.workspace = first.workspace
         self._res = nat.StepResult()
@@ -469,11 +513,11 @@ class ShardedDevice:
         self.comm.halo(strips, _STATE, 2, self.stream)
         for r in order:
             strips[r].phase(nat.PH_STAGE)
-        self.comm.pipeline(strips, nat.PH_SOLVE1F, nat.PH_SOLVE1B, self.stream)
+        self._ysolve(1)
         self.comm.halo(strips, _PENDING_PQ, 1, self.stream)
         for r in order:
             strips[r].phase(nat.PH_CORRECT)
-        self.comm.pipeline(strips, nat.PH_SOLVE2F, nat.PH_SOLVE2B, self.stream)
+        self._ysolve(2)
         parts = []
         for r in order:
             _, res = strips[r].phase(nat.PH_FINAL)
@@ -488,6 +532,23 @@ class ShardedDevice:
             out.state_bad[k] = m["state_bad"][k]
         rc = nat.BSQ_ERR_SINGULAR if self.singular else nat.BSQ_OK
         return rc, out
+
+    def _ysolve(self, solve: int):
+        """The line solves of one phase: x rows are local; y columns continue
+        across strips (rank pipeline) or are coupled afterwards (spike)."""
+        ph_f, ph_b = (nat.PH_SOLVE1F, nat.PH_SOLVE1B) if solve == 1 else \
+            (nat.PH_SOLVE2F, nat.PH_SOLVE2B)
+        if not self.spike:
+            self.comm.pipeline(self.strips, ph_f, ph_b, self.stream)
+            return
+        for r in sorted(self.strips):
+            self.strips[r].phase(ph_f)
+        if solve == 2 and not self.cross:
+            return
+        yb = self.comm.spike_bounds(self.strips, nat.ARR_Q_NEW if solve == 1 else nat.ARR_Q2,
+                                    self.stream)
+        for r, s in self.strips.items():
+            s.spike_fix(solve, yb[r])
 
     def commit(self):
         for s in self.strips.values():
@@ -523,17 +584,19 @@ class ShardedSimulator(Simulator):
     objects; every API is the Simulator's.
     """
 
-    def __init__(self, *args, world: int | None = None, comm=None, **kw):
+    def __init__(self, *args, world: int | None = None, comm=None, coupling: str = "pipeline",
+                 **kw):
         if comm is None:
             comm = LocalComm(world or 1)
         self._comm = comm
         self._world = comm.world
+        self._coupling = coupling
         super().__init__(*args, **kw)
 
     def _make_device(self, desc, bathy, device):
         if self.solver != "thomas":
             raise NotImplementedError("sharded solves use the Thomas pipeline")
-        return ShardedDevice(self, desc, bathy, device, self._world, self._comm)
+        return ShardedDevice(self, desc, bathy, device, self._world, self._comm, self._coupling)
 
     @property
     def stream(self):

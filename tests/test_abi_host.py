@@ -36,7 +36,7 @@ def test_library_exports_every_header_symbol():
 
 def test_struct_layouts_match_header_sizes():
     # sizes computed from the C declarations (x86-64 natural alignment)
-    assert ctypes.sizeof(nat.Desc) == 72 + 12 * 8 + 16  # 17 int32 + pad, 12 doubles, 4 int32
+    assert ctypes.sizeof(nat.Desc) == 72 + 12 * 8 + 24  # 17 int32 + pad, 12 doubles, 6 int32
     assert ctypes.sizeof(nat.Static) == 7 * 8
     assert ctypes.sizeof(nat.StepResult) == 5 * 8 + 8 * 8
     assert ctypes.sizeof(nat.StepParams) == 16 + 8 + 48 + 128 + 32

@@ -63,3 +63,46 @@ def test_split_rows_and_bands():
     assert strip_band(9, 6, 10, 5) == (0, 5, 1)
     assert strip_band(9, 6, 5, 5) == (4, 1, 0)
     assert strip_band(9, 6, 0, 5) == (0, 0, 0)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_spike_coupled_strips_match_single_gpu(world):
+    """coupling="spike" (partitioned y-solves, ranks concurrent): the same
+    solution up to rounding.  Bar: <= 1e-12 relative after 30
+    adaptive steps, and the same dt sequence to 1e-12."""
+    case = make_case("C4", scale=8)
+    one = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
+                            stepper.TimeController(dt_init=case.dt_init), phys=case.phys)
+    sp = ShardedSimulator(case.bathy, case.state.copy(), case.boundaries,
+                          stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
+                          world=world, coupling="spike")
+    for _ in range(30):
+        a, b = one.advance(), sp.advance()
+        assert b.dt == pytest.approx(a.dt, rel=1e-12)
+        assert b.max_speed == pytest.approx(a.max_speed, rel=1e-12)
+    sa, sb = one.state, sp.state
+    assert _rel(sb.w[II], sa.w[II]) <= 1e-12
+    # momenta against the larger of the two fields (Q is ~0 in 1-D-like parts)
+    scale = max(np.linalg.norm(sa.p[II]), np.linalg.norm(sa.q[II]))
+    for f in ("p", "q"):
+        assert np.linalg.norm(getattr(sb, f)[II] - getattr(sa, f)[II]) / scale <= 1e-12, f
+
+
+def test_spike_coupled_strips_golden_maker_sponge():
+    """Sponges on N/S rows split across strips, maker on the west edge: the
+    reference's own run to <= 1e-12 after 200 steps, same step count."""
+    z = gc.load("maker_sponge")
+    bathy, state, bounds, phys, ckw, skw = gc.inputs(z)
+    sim = ShardedSimulator(bathy, state, bounds, stepper.TimeController(**ckw), phys=phys,
+                           world=4, coupling="spike", **skw)
+    dts = [sim.advance().dt for _ in range(int(z["steps"]))]
+    assert np.allclose(dts, z["records"][:, 2], rtol=1e-12, atol=0)
+    st = sim.state
+    assert _rel(st.w[II], z["w"][II]) <= 1e-12
+    scale = max(np.linalg.norm(z["p"][II]), np.linalg.norm(z["q"][II]))
+    for f in ("p", "q"):
+        assert np.linalg.norm(getattr(st, f)[II] - z[f][II]) / scale <= 1e-12, f
