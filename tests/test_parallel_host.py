@@ -67,6 +67,10 @@ def run_local():
     return {r: ({a: t.clone() for a, t in s.f.items()}, s.col.clone()) for r, s in strips.items()}
 
 
+def _spike_coef(rank):
+    return np.arange(4 * NX, dtype=np.float64).reshape(4, NX) * (rank + 1) + 0.125
+
+
 def _worker(rank, port, out_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -101,8 +105,11 @@ def _worker(rank, port, out_q):
         else:
             got_tail = comm.get_tail(tails, 1, NX)
         any_flag = comm.any_flag([rank == 1])
+        # spike coupling: static table once, first/last solved rows per solve
+        table = comm.gather_spike_table({rank: _spike_coef(rank)}, NX)
+        yb = comm.spike_bounds(strips, nat.ARR_Q_NEW, None)[rank].numpy().copy()
         out_q.put((rank, {a: t.numpy().copy() for a, t in s.f.items()}, s.col.numpy().copy(),
-                   red, [a.copy() for a in full], got_tail, any_flag))
+                   red, [a.copy() for a in full], got_tail, any_flag, table, yb))
     finally:
         dist.destroy_process_group()
 
@@ -164,6 +171,22 @@ def test_distcomm_gather_setup_tails_flags(dist_results):
             assert np.array_equal(a, b)
     assert np.array_equal(dist_results[1][4], np.arange(NX) * 0.5)
     assert dist_results[0][5] and dist_results[1][5]
+
+
+def test_distcomm_spike_exchange_matches_localcomm(dist_results):
+    ranges = split_rows(NY, WORLD)
+    strips = {r: FakeStrip(r, *ranges[r]) for r in range(WORLD)}
+    comm = LocalComm(WORLD)
+    comm.halo(strips, (nat.ARR_W, nat.ARR_P, nat.ARR_Q), 2, None)
+    comm.halo(strips, (nat.ARR_P_NEW, nat.ARR_Q_NEW), 1, None)
+    comm.pipeline(strips, nat.PH_SOLVE1F, nat.PH_SOLVE1B, None)
+    want_tab = comm.gather_spike_table({r: _spike_coef(r) for r in range(WORLD)}, NX)
+    want_yb = comm.spike_bounds(strips, nat.ARR_Q_NEW, None)[0].numpy()
+    assert want_yb.shape == (WORLD, 2, NX)
+    for r in range(WORLD):
+        table, yb = dist_results[r][6], dist_results[r][7]
+        assert np.array_equal(table, want_tab)
+        assert np.array_equal(yb, want_yb)
 
 
 def test_combine_matches_reference_semantics():
