@@ -31,7 +31,6 @@ host-side logic is exercised with gloo on CPU by tests/test_parallel_host.py).
 
 from __future__ import annotations
 
-import ctypes
 import math
 
 import numpy as np
