@@ -104,6 +104,20 @@ typedef struct {
     double maker_eta_t[4], maker_flux_t[4]; /* maker_surface_flux at t     */
     double maker_eta_n[4], maker_flux_n[4]; /* maker_surface_flux at t+dt */
     const double *sponge_fac[4];            /* host, sponge_len[s] factors exp(-lambda dt) */
+    /* Speculation (whole grids; 0 = off).  With the controller state below,
+     * bsq_step queues the NEXT step's ghost and stage kernels right behind
+     * this step's finalize, with dt and weights from a device copy of the
+     * controller (stepper.py:304-312, multistep.py:31-228), so they overlap
+     * the host's turn-around.  The next bsq_step uses them only if this step
+     * was committed and its own dt, scheme, weights and maker values at t
+     * equal the speculated ones bit for bit; otherwise it relaunches them. */
+    int32_t spec;
+    int32_t adaptive;          /* TimeController.mode == "adaptive" */
+    int64_t step_index;        /* this step's index (before the increment) */
+    double cfl_target, alpha, dt_min, dt_max, dt_init;
+    double chain;              /* lazy-EMA chain before this step's update */
+    double dt_fixed;           /* controller dt in "fixed" mode */
+    double dt_prev;            /* the previous step's dt */
 } bsq_step_params;
 
 /* Per-step device reductions, returned to the host. */

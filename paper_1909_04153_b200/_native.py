@@ -59,7 +59,13 @@ class StepParams(ctypes.Structure):
                 ("sc", ctypes.c_double), ("sp", ctypes.c_double), ("sp2", ctypes.c_double),
                 ("maker_eta_t", ctypes.c_double * 4), ("maker_flux_t", ctypes.c_double * 4),
                 ("maker_eta_n", ctypes.c_double * 4), ("maker_flux_n", ctypes.c_double * 4),
-                ("sponge_fac", _dp * 4)]
+                ("sponge_fac", _dp * 4),
+                ("spec", ctypes.c_int32), ("adaptive", ctypes.c_int32),
+                ("step_index", ctypes.c_int64),
+                ("cfl_target", ctypes.c_double), ("alpha", ctypes.c_double),
+                ("dt_min", ctypes.c_double), ("dt_max", ctypes.c_double),
+                ("dt_init", ctypes.c_double), ("chain", ctypes.c_double),
+                ("dt_fixed", ctypes.c_double), ("dt_prev", ctypes.c_double)]
 
 
 class StepResult(ctypes.Structure):

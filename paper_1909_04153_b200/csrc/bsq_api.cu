@@ -48,12 +48,13 @@ enum Arr {
     A_BU, A_BV, A_US, A_VS, A_P2, A_Q2,
     A_BX, A_CX, A_BY, A_CY,  // diagonals for solver="cr"
     A_SPV, A_SPW,            // BSQ_Y_SPIKE: south / north coupling spikes
+    A_W2,                    // third w buffer: the speculative next stage writes here
     A_HIST0,  // 4 slots x 5 fields follow
     A_COUNT = A_HIST0 + 20
 };
 
 enum Small { S_CXL, S_CYL, S_FAC, S_PAR, S_RES, S_PART, S_CNT, S_DWIN, S_DWOUT, S_XIN, S_XOUT,
-             S_SPBT, S_COUNT };
+             S_SPBT, S_PAR2, S_FRAME, S_COUNT };
 
 bool spike_mode(const bsq_desc *d) {
     return d->y_coupling == BSQ_Y_SPIKE && (d->south_internal || d->north_internal);
@@ -96,7 +97,8 @@ size_t layout_bytes(const bsq_desc *d, size_t offs[A_COUNT + S_COUNT], int *fac_
                                    sizeof(DevParams), sizeof(DevResult),
                                    sizeof(Partial) * (size_t)final_blocks(d->nx, d->ny), 256,
                                    sizeof(T) * d->nx, sizeof(T) * d->nx, sizeof(T) * d->nx,
-                                   sizeof(T) * d->nx, sizeof(T) * 2 * d->nx};
+                                   sizeof(T) * d->nx, sizeof(T) * 2 * d->nx, sizeof(DevParams),
+                                   sizeof(T) * frame_elems(d->nx, d->ny)};
     for (int k = 0; k < S_COUNT; k++) {
         offs[A_COUNT + k] = off;
         off += align256(small[k]);
@@ -194,6 +196,29 @@ struct Engine : EngineBase {
     T *hstage = nullptr;           // pinned conversion staging (fp32 only): one padded field
     int fac_stride = 0, nfinal = 0;
     int cur = 0, head = 3, nlev = 0, pend_slot = 0;
+    // w has three buffers (committed, pending, spare) so the next step's
+    // stage can run before this step is committed; P and Q ping-pong
+    int wc_ = 0, wp_ = 1;
+    // speculation: dpar[pk] is this step's parameter block, dpar[pk ^ 1] the
+    // next step's as k_final's controller writes it
+    DevParams *dpar[2] = {nullptr, nullptr};
+    int pk = 0;
+    bool spec_pending = false;   // next step's ghost + stage are queued
+    bool spec_commit = false;    // ... and the step they follow was committed
+    bool spec_used = false;      // this step runs on them
+    bsq_step_params last_p{};    // parameters of the step that queued them
+    const bsq_step_params *cur_p = nullptr;  // the step in progress (bsq_step's argument)
+    SpecNext spec_h{};           // their scheme parameters (device controller)
+    // ghosts: the queued stage applies the next step's ghosts at t to the new
+    // state, whose user-visible ghosts are the reference's (applied at t+dt
+    // before the solves); those are saved and put back only if the state is
+    // read before the next step (which then re-applies the ghosts at t)
+    T *frame_w = nullptr, *frame_p = nullptr, *frame_q = nullptr;  // overwritten frame
+    bool frame_restored = false;
+    cudaEvent_t ev_res = nullptr;
+    cudaEvent_t ev_pre[kMaxEv] = {};
+    const char *pre_name[kMaxEv] = {};
+    int npre = 0;
     bool pending = false, singular = false, pos_pivots = true, timing = false;
     cudaEvent_t ev[kMaxEv] = {};
     const char *ev_name[kMaxEv] = {};
@@ -211,15 +236,20 @@ struct Engine : EngineBase {
     SolveMaps maps;                  // TMA descriptors (out slots patched per launch)
     CUtensorMap map_xout[3], map_yout[3];  // pending P/Q of state 0, state 1; P2/Q2
 
-    T *W(int s) { return arr[s ? A_W1 : A_W0]; }
+    static constexpr int kW[3] = {A_W0, A_W1, A_W2};
+    T *W(int s) { return arr[kW[s == cur ? wc_ : wp_]]; }  // W(cur) committed, W(1-cur) pending
+    T *Wspare() { return arr[kW[3 - wc_ - wp_]]; }
     T *Pp(int s) { return arr[s ? A_P1 : A_P0]; }
     T *Qq(int s) { return arr[s ? A_Q1 : A_Q0]; }
     T *H(int slot, int f) { return arr[A_HIST0 + slot * 5 + f]; }
 
     ~Engine() override {
         if (st) cudaStreamSynchronize(st);
-        for (int k = 0; k < kMaxEv; k++)
+        for (int k = 0; k < kMaxEv; k++) {
             if (ev[k]) cudaEventDestroy(ev[k]);
+            if (ev_pre[k]) cudaEventDestroy(ev_pre[k]);
+        }
+        if (ev_res) cudaEventDestroy(ev_res);
         if (hparams) cudaFreeHost(hparams);
         if (hres) cudaFreeHost(hres);
         if (hfac) cudaFreeHost(hfac);
@@ -512,7 +542,9 @@ struct Engine : EngineBase {
         cx_last = (T *)(base + offs[A_COUNT + S_CXL]);
         cy_last = (T *)(base + offs[A_COUNT + S_CYL]);
         for (int s = 0; s < 4; s++) fac[s] = (T *)(base + offs[A_COUNT + S_FAC]) + s * fac_stride;
-        dparams = (DevParams *)(base + offs[A_COUNT + S_PAR]);
+        dpar[0] = (DevParams *)(base + offs[A_COUNT + S_PAR]);
+        dpar[1] = (DevParams *)(base + offs[A_COUNT + S_PAR2]);
+        dparams = dpar[0];
         dres = (DevResult *)(base + offs[A_COUNT + S_RES]);
         part = (Partial *)(base + offs[A_COUNT + S_PART]);
         counter = (unsigned int *)(base + offs[A_COUNT + S_CNT]);
@@ -526,7 +558,11 @@ struct Engine : EngineBase {
         CU(cudaMallocHost(&hres, sizeof(DevResult)));
         CU(cudaMallocHost(&hfac, sizeof(T) * 4 * fac_stride));
         if (!F64) CU(cudaMallocHost(&hstage, sizeof(T) * (size_t)(d.ny + 4) * (d.nx + 4)));
-        for (int k = 0; k < kMaxEv; k++) CU(cudaEventCreate(&ev[k]));
+        for (int k = 0; k < kMaxEv; k++) {
+            CU(cudaEventCreate(&ev[k]));
+            CU(cudaEventCreate(&ev_pre[k]));
+        }
+        CU(cudaEventCreateWithFlags(&ev_res, cudaEventDisableTiming));
         set_consts();
         const int nx = d.nx, ny = d.ny;
         CU(cudaMemsetAsync(workspace, 0, need, st));  // ghost cells of scratch arrays stay defined
@@ -555,11 +591,25 @@ struct Engine : EngineBase {
         CU(cudaStreamSynchronize(st));
         pending = false;
         g_fresh = false;
+        spec_pending = false;
+        frame_w = frame_p = frame_q = nullptr;
         return BSQ_OK;
     }
+    T *frame_buf() { return (T *)(base + offs[A_COUNT + S_FRAME]); }
+
+    // a state about to be read shows the ghosts the reference leaves on it
+    void unframe(T *w, T *p, T *q) {
+        if (frame_w && frame_w == w && frame_p == p && frame_q == q) {
+            launch_frame(C, w, p, q, frame_buf(), 0, st);
+            frame_w = frame_p = frame_q = nullptr;
+            frame_restored = true;
+        }
+    }
+
     int download_state(int which, double *w, double *p, double *q) {
         if (which == 1 && !pending) return fail(BSQ_ERR_BAD_ARG, "no pending step");
         const int s = which == 1 ? 1 - cur : cur, ny = d.ny, nx = d.nx;
+        unframe(W(s), Pp(s), Qq(s));
         int rc;
         if ((rc = download_padded(w, W(s), ny + 4, nx + 4)) ||
             (rc = download_padded(p, Pp(s), ny + 4, nx + 4)) ||
@@ -595,6 +645,17 @@ struct Engine : EngineBase {
         h.sc = p->sc;
         h.sp = p->sp;
         h.sp2 = p->sp2;
+        h.spec = p->spec && !strip() ? 1 : 0;
+        h.adaptive = p->adaptive;
+        h.step_index = p->step_index;
+        h.cfl_target = p->cfl_target;
+        h.alpha = p->alpha;
+        h.dt_min = p->dt_min;
+        h.dt_max = p->dt_max;
+        h.dt_init = p->dt_init;
+        h.chain = p->chain;
+        h.dt_fixed = p->dt_fixed;
+        h.dt_prev = p->dt_prev;
         for (int s = 0; s < 4; s++) {
             h.gw_t[s] = d.ws + p->maker_eta_t[s];  // boundary.py:240 w_val = ws + eta
             h.gf_t[s] = p->maker_flux_t[s];
@@ -618,31 +679,56 @@ struct Engine : EngineBase {
     }
 
     StagePtrs<T> stage_ptrs(int slot) {
+        StagePtrs<T> A = stage_ptrs_on(W(cur), Pp(cur), Qq(cur), slot, head, (head + 3) % 4, W(1 - cur));
+        A.maxw = fold_req ? maxw : nullptr;
+        return A;
+    }
+
+    // the stage of the state (w, p, q) whose newest / middle stage levels are
+    // ring slots s1 / s2, writing slot `slot` and the predicted w into wn
+    StagePtrs<T> stage_ptrs_on(T *w, T *p, T *q, int slot, int s1, int s2, T *wn) {
         StagePtrs<T> A;
-        const int s = cur;
-        A.w = W(s);
-        A.p = Pp(s);
-        A.q = Qq(s);
+        A.w = w;
+        A.p = p;
+        A.q = q;
         A.be = arr[A_BE];
         A.dep = arr[A_DEP];
         A.ddx = arr[A_DDX];
         A.ddy = arr[A_DDY];
         A.bfx = arr[A_BFX];
         A.bfy = arr[A_BFY];
-        const int s1 = head, s2 = (head + 3) % 4;
         for (int f = 0; f < 5; f++) {
             A.h0[f] = H(slot, f);
             A.h1[f] = H(s1, f);
             A.h2[f] = H(s2, f);
         }
-        A.wn = W(1 - s);
+        A.wn = wn;
         A.bu = arr[A_BU];
         A.bv = arr[A_BV];
         A.us = arr[A_US];
         A.vs = arr[A_VS];
         A.bad = dres->stage_bad;
-        A.maxw = fold_req ? maxw : nullptr;
+        A.maxw = nullptr;
         return A;
+    }
+
+    static bool same_bits(double a, double b) { return std::memcmp(&a, &b, sizeof a) == 0; }
+
+    // the queued ghost + stage are this step's: the previous step was
+    // committed and every input they consumed equals this step's
+    bool spec_matches(const bsq_step_params *p) const {
+        if (!(spec_pending && spec_commit && spec_h.valid && p->spec)) return false;
+        if (!same_bits(p->dt, spec_h.dt) || (p->euler != 0) != (spec_h.euler != 0)) return false;
+        if (!p->euler &&
+            !(same_bits(p->wc, spec_h.wc) && same_bits(p->wp, spec_h.wp) &&
+              same_bits(p->wp2, spec_h.wp2) && same_bits(p->sc, spec_h.sc) &&
+              same_bits(p->sp, spec_h.sp) && same_bits(p->sp2, spec_h.sp2)))
+            return false;
+        for (int s = 0; s < 4; s++)
+            if (!same_bits(p->maker_eta_t[s], last_p.maker_eta_n[s]) ||
+                !same_bits(p->maker_flux_t[s], last_p.maker_flux_n[s]))
+                return false;
+        return true;
     }
 
     SolvePtrs<T> solve_ptrs(int nxt_state) {
@@ -708,6 +794,28 @@ struct Engine : EngineBase {
         const int fwd_mode = piped ? SOLVE_X_YFWD : SOLVE_FULL;
         switch (ph) {
         case BSQ_PH_GHOST: {
+            cur_p = p;
+            spec_used = !strip() && spec_matches(p);
+            spec_pending = false;
+            if (spec_used) {  // the stage already ran (on dpar[pk ^ 1])
+                pk ^= 1;
+                dparams = dpar[pk];
+                int rc = stage_params(p);  // the rest of this step's parameters
+                if (rc) return rc;
+                nev = npre;
+                for (int k = 0; k < npre; k++) {
+                    std::swap(ev[k], ev_pre[k]);
+                    ev_name[k] = pre_name[k];
+                }
+                // the committed state carries the ghosts at t (the reference
+                // applies them in place) -- unless a read put the old ones back
+                if (frame_restored)
+                    launch_ghost(C, dparams, 0, W(cur), Pp(cur), Qq(cur), W(cur), Pp(cur), Qq(cur),
+                                 st);
+                frame_w = frame_p = frame_q = nullptr;
+                frame_restored = false;
+                break;
+            }
             int rc = stage_params(p);
             if (rc) return rc;
             CU(cudaMemsetAsync(dres, 0xFF, sizeof(DevResult), st));
@@ -718,9 +826,11 @@ struct Engine : EngineBase {
             break;
         }
         case BSQ_PH_STAGE:
-            launch_stage(C, dparams, stage_ptrs(slot), 1, st);
-            fold_req = false;
-            ev_mark("stage");
+            if (!spec_used) {
+                launch_stage(C, dparams, stage_ptrs(slot), 1, st);
+                fold_req = false;
+                ev_mark("stage");
+            }
             launch_ghost(C, dparams, 1, W(nxt), Pp(cur), Qq(cur), W(nxt), Pp(nxt), Qq(nxt), st);
             ev_mark("ghost_n");
             break;
@@ -790,13 +900,47 @@ struct Engine : EngineBase {
         F.goff = d_goff;
         F.ng = ng;
         F.gval = d_gval;
+        const bool spec = hparams->spec && !strip() && !fold_req;
+        F.P = dparams;
+        F.pnext = spec ? dpar[pk ^ 1] : nullptr;
         launch_final(C, F, st);
         ev_mark("final");
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
         if (ng)
             CU(cudaMemcpyAsync(h_gstage, d_gval, sizeof(T) * 3 * ng, cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
+        CU(cudaEventRecord(ev_res, st));
+        if (spec) {
+            // the next step's ghost at t and stage, on this step's new state,
+            // behind the result copy: they overlap the host's turn-around
+            last_p = *cur_p;
+            CU(cudaMemsetAsync(dres, 0xFF, sizeof(DevResult), st));
+            DevParams *pn = dpar[pk ^ 1];
+            npre = 0;
+            auto pre = [&](const char *nm) {
+                if (!timing || npre >= kMaxEv) return;
+                pre_name[npre] = nm;
+                cudaEventRecord(ev_pre[npre++], st);
+            };
+            // the new state keeps the ghosts the reference leaves on it
+            // (applied at t+dt before the solves); the queued stage needs the
+            // ones at t_{n+1}: save, apply, run, restore
+            pre("start");
+            launch_frame(C, W(nxt), Pp(nxt), Qq(nxt), frame_buf(), 1, st);
+            frame_w = W(nxt), frame_p = Pp(nxt), frame_q = Qq(nxt);
+            frame_restored = false;
+            launch_ghost(C, pn, 0, W(nxt), Pp(nxt), Qq(nxt), W(nxt), Pp(nxt), Qq(nxt), st);
+            pre("ghost_t");
+            launch_stage(C, pn, stage_ptrs_on(W(nxt), Pp(nxt), Qq(nxt), (slot + 1) % 4, slot, head,
+                                              Wspare()), 1, st);
+            pre("stage");
+            CU(cudaGetLastError());
+            spec_pending = true;
+            spec_commit = false;
+        }
+        CU(cudaEventSynchronize(ev_res));
+        spec_h = hres->next;
+        if (!spec) spec_h.valid = 0;
         for (int k = 0; k < 3 * ng; k++) g_pend[k] = double(h_gstage[k]);
         if (timing) {
             last_n = nev - 1;
@@ -846,9 +990,9 @@ struct Engine : EngineBase {
     int array_layout(int which, size_t *off, int *pitch, int *xo, int *eb) {
         const T *ptr = nullptr;
         switch (which) {
-        case BSQ_ARR_W: ptr = W(cur); break;
-        case BSQ_ARR_P: ptr = Pp(cur); break;
-        case BSQ_ARR_Q: ptr = Qq(cur); break;
+        case BSQ_ARR_W: unframe(W(cur), Pp(cur), Qq(cur)); ptr = W(cur); break;
+        case BSQ_ARR_P: unframe(W(cur), Pp(cur), Qq(cur)); ptr = Pp(cur); break;
+        case BSQ_ARR_Q: unframe(W(cur), Pp(cur), Qq(cur)); ptr = Qq(cur); break;
         case BSQ_ARR_W_NEW: ptr = W(1 - cur); break;
         case BSQ_ARR_P_NEW: ptr = Pp(1 - cur); break;
         case BSQ_ARR_Q_NEW: ptr = Qq(1 - cur); break;
@@ -869,9 +1013,13 @@ struct Engine : EngineBase {
     int commit() {
         if (!pending) return fail(BSQ_ERR_BAD_ARG, "no pending step to commit");
         cur = 1 - cur;
+        const int old_wc = wc_;
+        wc_ = wp_;
+        wp_ = 3 - old_wc - wc_;  // the spare: where a queued next stage wrote w
         head = pend_slot;
         if (nlev < 3) nlev++;
         pending = false;
+        if (spec_pending) spec_commit = true;
         g_com = g_pend;
         g_fresh = ng > 0;
         return BSQ_OK;
@@ -941,6 +1089,11 @@ struct Engine : EngineBase {
         }
         case BSQ_MAX_FOLD:
             if (!maxw) return fail(BSQ_ERR_BAD_ARG, "max tracker not enabled");
+            if (spec_pending) {  // the next stage is already queued: fold now
+                launch_fold_max(C, W(cur), maxw, st);
+                CU(cudaGetLastError());
+                return BSQ_OK;
+            }
             fold_req = true;  // the next stage kernel folds the committed state
             return BSQ_OK;
         case BSQ_MAX_FLUSH:
@@ -966,6 +1119,7 @@ struct Engine : EngineBase {
 
     // -- kernel-level seams ----------------------------------------------------------
     int stage_rates(double *outs[5]) {
+        spec_pending = false;
         CU(cudaMemsetAsync(dres, 0xFF, sizeof(DevResult), st));
         const int slot = (head + 1) % 4;
         launch_stage(C, dparams, stage_ptrs(slot), 0, st);
@@ -983,6 +1137,7 @@ struct Engine : EngineBase {
                        const double *qgs, const double *qgn, double *pout, double *qout) {
         if (d.solver != BSQ_CR && singular)
             return fail(BSQ_ERR_SINGULAR, "singular tridiagonal system: zero pivot");
+        spec_pending = false;
         const int nxt = 1 - cur, nx = d.nx, ny = d.ny;
         int rc;
         if ((rc = upload_interior(arr[A_US], us)) || (rc = upload_interior(arr[A_VS], vs)))
@@ -1030,6 +1185,8 @@ struct Engine : EngineBase {
     }
 
     int fill_ghosts(const double *eta, const double *flux) {
+        spec_pending = false;
+        frame_w = frame_p = frame_q = nullptr;
         DevParams &h = *hparams;
         for (int s = 0; s < 4; s++) {
             h.gw_t[s] = d.ws + eta[s];

@@ -77,6 +77,80 @@ __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, 
     if (double(h) > r.depth) r.depth = double(h);
 }
 
+// Python's min / max of two floats: the first argument unless the second is
+// strictly smaller / larger
+__device__ __forceinline__ double py_min(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double py_max(double a, double b) { return b > a ? b : a; }
+
+// The next step's scheme parameters from this step's max CFL rate: the host
+// controller (stepper.py cfl_candidate / lazy_ema / dt update) and the
+// clamped AB3 / VFD weights (multistep.py StepTriple.validated, ab3_weights,
+// vfd_weights, increment_weights), same operations in the same order.  The
+// host recomputes all of it and only uses the speculated stage if every
+// value agrees bit for bit.
+__device__ void spec_next(const DevParams &P, double max_rate, DevParams &N, SpecNext &o) {
+    double dt;
+    if (P.adaptive) {
+        const double cand = max_rate <= 0.0
+                                ? P.dt_max
+                                : py_min(py_max(P.cfl_target / max_rate, P.dt_min), P.dt_max);
+        const double chain = cand <= P.chain ? cand : P.alpha * cand + (1.0 - P.alpha) * P.chain;
+        dt = P.step_index + 1 >= 3 ? chain : P.dt_init;
+    } else {
+        dt = P.dt_fixed;
+    }
+    const int euler = P.step_index + 1 < 3;
+    double w0 = 0, w1 = 0, w2 = 0, s0 = 0, s1 = 0, s2 = 0;
+    if (!euler) {
+        double a = P.dt, b = P.dt_prev;  // StepTriple(dt, dt_prev, dt_prev2), clamped
+        const double r1 = dt / a, r2 = a / b;
+        const double lo = 0.1 * (1.0 - 1e-12), hi = 10.0 * (1.0 + 1e-12);
+        if (!(lo <= r1 && r1 <= hi && lo <= r2 && r2 <= hi)) {
+            a = py_min(py_max(a, dt / 10.0), dt / 0.1);
+            b = py_min(py_max(b, a / 10.0), a / 0.1);
+        }
+        if (dt == a && a == b) {
+            w0 = (23.0 / 12.0) * dt;
+            w1 = (-16.0 / 12.0) * dt;
+            w2 = (5.0 / 12.0) * dt;
+            s0 = 2.0;
+            s1 = -3.0;
+            s2 = 1.0;
+        } else {
+            w0 = (dt / 6.0) * (dt * (2.0 * dt + 6.0 * a + 3.0 * b) / (a * (a + b)) + 6.0);
+            w1 = -(dt / 6.0) * (dt * (2.0 * dt + 3.0 * a + 3.0 * b) / (a * b));
+            w2 = (dt / 6.0) * (dt * (2.0 * dt + 3.0 * a) / (b * (a + b)));
+            double n0, n1, n2, m0, m1, m2, o0, o1, o2;
+            if (a == b) {
+                const double h = a;
+                n0 = 1.5 / h, n1 = -2.0 / h, n2 = 0.5 / h;
+                m0 = 0.5 / h, m1 = 0.0, m2 = -0.5 / h;
+                o0 = -0.5 / h, o1 = 2.0 / h, o2 = -1.5 / h;
+            } else {
+                n0 = (2.0 * a + b) / (a * (a + b)), n1 = -(a + b) / (a * b), n2 = a / (b * (a + b));
+                m0 = b / (a * (a + b)), m1 = (a - b) / (a * b), m2 = -a / (b * (a + b));
+                o0 = -b / (a * (a + b)), o1 = (a + b) / (a * b), o2 = -(a + 2.0 * b) / (b * (a + b));
+            }
+            s0 = w0 * n0 + w1 * m0 + w2 * o0;
+            s1 = w0 * n1 + w1 * m1 + w2 * o1;
+            s2 = w0 * n2 + w1 * m2 + w2 * o2;
+        }
+    }
+    N.t = P.t + P.dt;
+    N.dt = dt;
+    N.euler = euler;
+    N.wc = w0, N.wp = w1, N.wp2 = w2, N.sc = s0, N.sp = s1, N.sp2 = s2;
+    for (int s = 0; s < 4; s++) {  // the next step's ghosts at t are this step's at t + dt
+        N.gw_t[s] = P.gw_n[s];
+        N.gf_t[s] = P.gf_n[s];
+    }
+    N.spec = 0;
+    o.dt = dt;
+    o.euler = euler;
+    o.valid = 1;
+    o.wc = w0, o.wp = w1, o.wp2 = w2, o.sc = s0, o.sp = s1, o.sp2 = s2;
+}
+
 template <class T>
 __global__ void __launch_bounds__(FT) k_final(Consts<T> C, FinalPtrs<T> F) {
     __shared__ bool am_last;
@@ -188,6 +262,7 @@ __global__ void __launch_bounds__(FT) k_final(Consts<T> C, FinalPtrs<T> F) {
         F.res->max_dev = a.nan ? (double)NAN : a.dev;
         F.res->clamped = a.clamp;
         *F.counter = 0u;
+        if (F.pnext && F.P->spec) spec_next(*F.P, a.rate, *F.pnext, F.res->next);
     }
 }
 

@@ -87,6 +87,50 @@ __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which,
     }
 }
 
+// The 2-cell ghost frame of (w, p, q): rows 0, 1, ny+2, ny+3 over the padded
+// width, then columns 0, 1, nx+2, nx+3 over the interior rows.  save = 1
+// copies frame -> buf, 0 copies buf -> frame.  Used to keep a state's
+// user-visible ghosts while a queued next stage runs on ghosts at t_{n+1}.
+template <class T>
+__global__ void k_frame(Consts<T> C, T *w, T *p, T *q, T *buf, int save) {
+    const Layout L = C.L;
+    const int W = L.nx + 4, nrow = 4 * W, n = nrow + 4 * L.ny;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int J, I;
+    if (k < nrow) {
+        const int r = k / W;
+        J = r < 2 ? r : L.ny + r;  // 0, 1, ny+2, ny+3
+        I = k - r * W;
+    } else {
+        const int kk = k - nrow, c = kk / L.ny;
+        J = GL + (kk - c * L.ny);
+        I = c < 2 ? c : L.nx + c;  // 0, 1, nx+2, nx+3
+    }
+    const long o = L.at(J, I);
+    T *f[3] = {w, p, q};
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        if (save)
+            buf[(long)a * n + k] = f[a][o];
+        else
+            f[a][o] = buf[(long)a * n + k];
+    }
+}
+
+template <class T>
+void launch_frame(const Consts<T> &C, T *w, T *p, T *q, T *buf, int save, cudaStream_t st) {
+    const int n = 4 * (C.L.nx + 4) + 4 * C.L.ny;
+    k_frame<T><<<(n + 255) / 256, 256, 0, st>>>(C, w, p, q, buf, save);
+}
+
+size_t frame_elems(int nx, int ny) { return 3 * ((size_t)4 * (nx + 4) + (size_t)4 * ny); }
+
+template void launch_frame<double>(const Consts<double> &, double *, double *, double *, double *,
+                                   int, cudaStream_t);
+template void launch_frame<float>(const Consts<float> &, float *, float *, float *, float *, int,
+                                  cudaStream_t);
+
 template <class T>
 void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
                   const T *sq, T *dw, T *dp, T *dq, cudaStream_t st) {

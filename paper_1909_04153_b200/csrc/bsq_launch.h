@@ -76,11 +76,16 @@ struct FinalPtrs {
     const long long *goff;          // gauge cells (element offsets), gathered by the last CTA
     int ng;
     T *gval;                        // ng x (w, P, Q) of the new state
+    const DevParams *P;             // this step's parameters (controller inputs)
+    DevParams *pnext;               // speculation: the next step's ghost/stage parameters
 };
 
 template <class T>
 void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
                   const T *sq, T *dw, T *dp, T *dq, cudaStream_t st);
+template <class T>
+void launch_frame(const Consts<T> &C, T *w, T *p, T *q, T *buf, int save, cudaStream_t st);
+size_t frame_elems(int nx, int ny);
 template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
                   cudaStream_t st);

@@ -237,6 +237,7 @@ class Simulator:
         self._chain = controller.dt_init
         self._extrema = self._dev.speed_extrema()
         self._params = nat.StepParams()
+        self.speculate = True  # queue the next stage behind each step (bsq_step_params.spec)
         # maker components as (amplitude, omega, k, phase) rows for the
         # native per-step sums (bsq_maker_sums == boundary.maker_surface_flux)
         self._maker_rows = [
@@ -391,6 +392,14 @@ class Simulator:
         c = self.controller
         pr = self._params
         pr.t, pr.dt, pr.euler = t, dt_used, 1 if euler else 0
+        # controller state: lets the library queue the next step's stage
+        # behind this one (verified against the host's own values next step)
+        pr.spec = 1 if self.speculate else 0
+        pr.adaptive = 1 if c.mode == "adaptive" else 0
+        pr.step_index = c.step_index
+        pr.cfl_target, pr.alpha, pr.dt_min, pr.dt_max = c.cfl_target, c.alpha, c.dt_min, c.dt_max
+        pr.dt_init, pr.chain, pr.dt_fixed = c.dt_init, self._chain, c.dt
+        pr.dt_prev = c.dt_prev if math.isfinite(c.dt_prev) else 0.0
         if not euler:
             steps = multistep.StepTriple(dt_used, c.dt_prev, c.dt_prev2)
             w = multistep.ab3_weights(steps, ratio_policy="clamp")

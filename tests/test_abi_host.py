@@ -39,7 +39,7 @@ def test_struct_layouts_match_header_sizes():
     assert ctypes.sizeof(nat.Desc) == 72 + 12 * 8 + 24  # 17 int32 + pad, 12 doubles, 6 int32
     assert ctypes.sizeof(nat.Static) == 7 * 8
     assert ctypes.sizeof(nat.StepResult) == 5 * 8 + 8 * 8
-    assert ctypes.sizeof(nat.StepParams) == 16 + 8 + 48 + 128 + 32
+    assert ctypes.sizeof(nat.StepParams) == 16 + 8 + 48 + 128 + 32 + 8 + 8 + 8 * 8
 
 
 def test_workspace_query_needs_no_gpu():

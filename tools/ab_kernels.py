@@ -24,11 +24,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--precision", default="fp64")
 ap.add_argument("--case", default="C4")
+ap.add_argument("--no-spec", action="store_true", help="do not queue the next stage early")
 a = ap.parse_args()
 case = make_case(a.case)
 sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
                         stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
                         precision=a.precision)
+sim.speculate = not a.no_spec
 for _ in range(4):
     sim.advance()
 sim._dev.set_timing(True)
@@ -42,5 +44,6 @@ for _ in range(a.steps):
     n += 1
 torch.cuda.synchronize()
 wall = (time.perf_counter() - t0) / n * 1e3
-print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "step_ms_wall": round(wall, 4),
+print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "spec": not a.no_spec,
+                  "step_ms_wall": round(wall, 4),
                   **{k: round(v / n, 4) for k, v in acc.items()}}))
