@@ -262,7 +262,8 @@ int bsq_maker_sums(const double *comps, int n, double t, double *out);
  * device times (ms) and names, in launch order. */
 int bsq_set_timing(bsq_ctx *ctx, int enable);
 int bsq_kernel_times(bsq_ctx *ctx, int max_n, float *ms, const char **names, int *n_out);
-/* number of kernels one bsq_step launches */
+/* number of kernels the last bsq_step launched (with speculation this
+ * includes the next step's queued ghost + stage, and excludes its own) */
 int bsq_kernels_per_step(bsq_ctx *ctx);
 
 #ifdef __cplusplus

@@ -219,6 +219,7 @@ struct Engine : EngineBase {
     cudaEvent_t ev_pre[kMaxEv] = {};
     const char *pre_name[kMaxEv] = {};
     int npre = 0;
+    long long step_launches = 0;  // kernels queued by the current / last bsq_step
     bool pending = false, singular = false, pos_pivots = true, timing = false;
     cudaEvent_t ev[kMaxEv] = {};
     const char *ev_name[kMaxEv] = {};
@@ -795,6 +796,7 @@ struct Engine : EngineBase {
         switch (ph) {
         case BSQ_PH_GHOST: {
             cur_p = p;
+            step_launches = 0;
             spec_used = !strip() && spec_matches(p);
             spec_pending = false;
             if (spec_used) {  // the stage already ran (on dpar[pk ^ 1])
@@ -809,9 +811,11 @@ struct Engine : EngineBase {
                 }
                 // the committed state carries the ghosts at t (the reference
                 // applies them in place) -- unless a read put the old ones back
-                if (frame_restored)
+                if (frame_restored) {
+                    ++step_launches;
                     launch_ghost(C, dparams, 0, W(cur), Pp(cur), Qq(cur), W(cur), Pp(cur), Qq(cur),
                                  st);
+                }
                 frame_w = frame_p = frame_q = nullptr;
                 frame_restored = false;
                 break;
@@ -821,20 +825,24 @@ struct Engine : EngineBase {
             CU(cudaMemsetAsync(dres, 0xFF, sizeof(DevResult), st));
             nev = 0;
             ev_mark("start");
+            ++step_launches;
             launch_ghost(C, dparams, 0, W(cur), Pp(cur), Qq(cur), W(cur), Pp(cur), Qq(cur), st);
             ev_mark("ghost_t");
             break;
         }
         case BSQ_PH_STAGE:
             if (!spec_used) {
+                ++step_launches;
                 launch_stage(C, dparams, stage_ptrs(slot), 1, st);
                 fold_req = false;
                 ev_mark("stage");
             }
+            ++step_launches;
             launch_ghost(C, dparams, 1, W(nxt), Pp(cur), Qq(cur), W(nxt), Pp(nxt), Qq(nxt), st);
             ev_mark("ghost_n");
             break;
         case BSQ_PH_SOLVE1F:
+            ++step_launches;
             if (d.solver == BSQ_CR)
                 launch_cr(C, cr_ptrs(1, nxt), st);
             else
@@ -843,18 +851,21 @@ struct Engine : EngineBase {
             break;
         case BSQ_PH_SOLVE1B:
             if (piped) {
+                ++step_launches;
                 launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st, SOLVE_YBWD);
                 ev_mark("solve1b");
             }
             break;
         case BSQ_PH_CORRECT:
             if (d.cross_correction) {
+                ++step_launches;
                 launch_correct(C, correct_ptrs(slot, nxt), st);
                 ev_mark("correct");
             }
             break;
         case BSQ_PH_SOLVE2F:
             if (d.cross_correction) {
+                ++step_launches;
                 if (d.solver == BSQ_CR)
                     launch_cr(C, cr_ptrs(2, nxt), st);
                 else
@@ -864,6 +875,7 @@ struct Engine : EngineBase {
             break;
         case BSQ_PH_SOLVE2B:
             if (d.cross_correction && piped) {
+                ++step_launches;
                 launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st, SOLVE_YBWD);
                 ev_mark("solve2b");
             }
@@ -903,6 +915,7 @@ struct Engine : EngineBase {
         const bool spec = hparams->spec && !strip() && !fold_req;
         F.P = dparams;
         F.pnext = spec ? dpar[pk ^ 1] : nullptr;
+        ++step_launches;
         launch_final(C, F, st);
         ev_mark("final");
         CU(cudaGetLastError());
@@ -926,11 +939,14 @@ struct Engine : EngineBase {
             // (applied at t+dt before the solves); the queued stage needs the
             // ones at t_{n+1}: save, apply, run, restore
             pre("start");
+            ++step_launches;
             launch_frame(C, W(nxt), Pp(nxt), Qq(nxt), frame_buf(), 1, st);
             frame_w = W(nxt), frame_p = Pp(nxt), frame_q = Qq(nxt);
             frame_restored = false;
+            ++step_launches;
             launch_ghost(C, pn, 0, W(nxt), Pp(nxt), Qq(nxt), W(nxt), Pp(nxt), Qq(nxt), st);
             pre("ghost_t");
+            ++step_launches;
             launch_stage(C, pn, stage_ptrs_on(W(nxt), Pp(nxt), Qq(nxt), (slot + 1) % 4, slot, head,
                                               Wspare()), 1, st);
             pre("stage");
@@ -1401,7 +1417,7 @@ int bsq_kernel_times(bsq_ctx *c, int max_n, float *ms, const char **names, int *
 
 int bsq_kernels_per_step(bsq_ctx *c) {
     if (!c) return 0;
-    return ENGINE(c, e->d.cross_correction ? 7 : 5);
+    return ENGINE(c, (int)(e->step_launches ? e->step_launches : (e->d.cross_correction ? 7 : 5)));
 }
 
 }  // extern "C"
