@@ -785,6 +785,19 @@ struct Engine : EngineBase {
 
     bool strip() const { return d.south_internal || d.north_internal; }
 
+    // The TMA unit bounds its tensor stores in 16-byte units of the inner
+    // dimension: when a row's nx elements end inside a unit (odd nx in fp64,
+    // nx % 4 != 0 in fp32) the solve's stores into the pending P / Q also
+    // write their first east ghost column.  The ghosts at t+dt are read
+    // afterwards (cross terms, second-solve folding), so re-apply them: same
+    // kernel, same inputs as the stage phase's fill.
+    bool tma_tail_clobbers() const { return (d.nx * (int)sizeof(T)) % 16 != 0; }
+    void reghost_after_tma(int nxt) {
+        if (!tma_tail_clobbers()) return;
+        ++step_launches;
+        launch_ghost(C, dparams, 1, W(nxt), Pp(cur), Qq(cur), W(nxt), Pp(nxt), Qq(nxt), st);
+    }
+
     // One phase of the step (include/bsq.h BSQ_PH_*).  For a whole grid the
     // y-line solves run complete inside the *F phases and the *B phases are
     // empty; for a strip they split at the rank boundary exchange.
@@ -843,16 +856,19 @@ struct Engine : EngineBase {
             break;
         case BSQ_PH_SOLVE1F:
             ++step_launches;
-            if (d.solver == BSQ_CR)
+            if (d.solver == BSQ_CR) {
                 launch_cr(C, cr_ptrs(1, nxt), st);
-            else
+            } else {
                 launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st, fwd_mode);
+                reghost_after_tma(nxt);
+            }
             ev_mark("solve1");
             break;
         case BSQ_PH_SOLVE1B:
             if (piped) {
                 ++step_launches;
                 launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st, SOLVE_YBWD);
+                reghost_after_tma(nxt);
                 ev_mark("solve1b");
             }
             break;
