@@ -56,6 +56,8 @@ def test_golden_run_bitwise(name):
         got, want = getattr(st, f)[II], z[f][II]
         assert rel_l2(got, want) <= REL_L2_TOL
         assert np.array_equal(got, want), f
+        # the padded arrays a caller sees, ghost frame included
+        assert np.array_equal(getattr(st, f), z[f]), f + " (padded)"
     assert sim.clamped_volume == pytest.approx(float(z["clamped_volume"]), rel=1e-12, abs=1e-300)
     if int(z["abort_step"]) >= 0:
         assert abort == (int(z["abort_step"]), float(z["abort_time"]), str(z["abort_msg"]))

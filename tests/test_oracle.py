@@ -36,6 +36,7 @@ def test_oracle_matches_reference_run_bitwise(name):
     st = sim.state
     for f in ("w", "p", "q"):
         assert np.array_equal(getattr(st, f)[II], z[f][II]), f
+        assert np.array_equal(getattr(st, f), z[f]), f + " (padded, ghost frame included)"
     assert sim.clamped_volume == pytest.approx(float(z["clamped_volume"]), rel=1e-12, abs=1e-300)
     if int(z["abort_step"]) >= 0:
         assert abort is not None and abort[0] == int(z["abort_step"])
