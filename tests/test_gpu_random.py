@@ -134,3 +134,59 @@ def test_random_configuration_sharded_bitwise_vs_oracle(seed):
     ii = bathy.grid.interior
     for f in ("w", "p", "q"):
         assert np.array_equal(getattr(sim.state, f)[ii], getattr(ora.state, f)[ii]), f
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("seed", [s for s in SEEDS if s % 4 == 1])
+def test_random_configuration_spike_strips_vs_oracle(seed):
+    """coupling="spike" on random configurations: <= 1e-12 relative to the
+    oracle after 30 steps (same dt sequence to 1e-12)."""
+    from paper_1909_04153_b200.parallel import ShardedSimulator
+    bathy, state, bounds, phys, ckw, skw = _config(seed)
+    skw["solver"] = "thomas"
+    world = 3 if bathy.grid.ny >= 15 else 2
+    if bathy.grid.ny < 5 * world:
+        pytest.skip("too few rows for the strips")
+    sim = ShardedSimulator(bathy, state.copy(), bounds, stepper.TimeController(**ckw),
+                           phys=phys, world=world, coupling="spike", **skw)
+    ora = orc.OracleSimulator(bathy, state.copy(), bounds, orc.OController(**ckw), phys=phys,
+                              **skw)
+    for k in range(30):
+        try:
+            a = sim.advance()
+        except stepper.InstabilityError:
+            return  # a configuration that blows up is not a coupling test
+        b = ora.advance()
+        assert a.dt == pytest.approx(b.dt, rel=1e-12), k
+    ii = bathy.grid.interior
+    sa, sb = sim.state, ora.state
+    assert _rel(sa.w[ii], sb.w[ii]) <= 1e-12
+    scale = max(np.linalg.norm(sb.p[ii]), np.linalg.norm(sb.q[ii]), 1e-300)
+    for f in ("p", "q"):
+        assert np.linalg.norm(getattr(sa, f)[ii] - getattr(sb, f)[ii]) / scale <= 1e-10, f
+
+
+@pytest.mark.parametrize("seed", [s for s in SEEDS if s % 4 == 2])
+def test_random_configuration_fp32_vs_oracle(seed):
+    """precision="fp32" on random configurations: eta rel-L2 <= 1e-4 against
+    the fp64 oracle after 30 steps (fixed dt, so both take the same steps);
+    3e-4 with solver="cr", whose fp32 reduction rounds more than Thomas."""
+    bathy, state, bounds, phys, ckw, skw = _config(seed)
+    ckw = dict(ckw, mode="fixed")
+    sim = stepper.Simulator(bathy, state.copy(), bounds, stepper.TimeController(**ckw),
+                            phys=phys, precision="fp32", **skw)
+    ora = orc.OracleSimulator(bathy, state.copy(), bounds, orc.OController(**ckw), phys=phys,
+                              **skw)
+    for _ in range(30):
+        try:
+            sim.advance()
+        except stepper.InstabilityError:
+            return
+        ora.advance()
+    ii = bathy.grid.interior
+    eta_a = sim.state.w[ii] - bathy.ws
+    eta_b = ora.state.w[ii] - bathy.ws
+    assert _rel(eta_a, eta_b) <= (1e-4 if skw["solver"] == "thomas" else 3e-4)
