@@ -221,6 +221,10 @@ struct Engine : EngineBase {
     int npre = 0;
     long long step_launches = 0;  // kernels queued by the current / last bsq_step
     bool pending = false, singular = false, pos_pivots = true, timing = false;
+    bool rden_inrange = true;  // every pivot's exponent in [-1000, 1000]: RN(1/den) on chip
+    int piv_flags() const {
+        return (pos_pivots ? PIV_POSITIVE : 0) | (rden_inrange ? PIV_RDEN_INRANGE : 0);
+    }
     cudaEvent_t ev[kMaxEv] = {};
     const char *ev_name[kMaxEv] = {};
     int nev = 0, last_n = 0;
@@ -357,7 +361,7 @@ struct Engine : EngineBase {
         std::vector<T> ay(E, T(0)), deny(E, T(1)), rdeny(E, T(-1)), cwy(E, T(0));
         std::vector<T> cxl(ny), cyl(nx);
         const double six_dx = 6.0 * d.dx, six_dy = 6.0 * d.dy;
-        bool sing = false, pos = true;
+        bool sing = false, pos = true, inrange = true;
         auto put = [&](std::vector<T> &A, std::vector<T> &D, std::vector<T> &R,
                        std::vector<T> &CW, long o, double a, double den, double cw) {
             A[o] = T(a);
@@ -367,6 +371,8 @@ struct Engine : EngineBase {
             CW[o] = T(cw);
             if (!(dT > T(0))) pos = false;
             if (den == 0.0) sing = true;
+            const double ad = std::fabs(double(dT));  // rcp_rn_inrange's domain
+            if (!(ad >= 0x1p-1000 && ad <= 0x1p1000)) inrange = false;
         };
         for (int j = 0; j < ny; j++) {  // x rows
             double cw_prev = 0.0;
@@ -408,6 +414,7 @@ struct Engine : EngineBase {
         }
         singular = sing;
         pos_pivots = pos;
+        rden_inrange = inrange;
         if (spike) make_spikes(ay, deny, cwy, cyl);
         const size_t B = sizeof(T) * E;
         const std::vector<T> *src[12] = {&ax, &denx, &rdenx, &cwx, &ay, &deny, &rdeny, &cwy,
@@ -859,7 +866,7 @@ struct Engine : EngineBase {
             if (d.solver == BSQ_CR) {
                 launch_cr(C, cr_ptrs(1, nxt), st);
             } else {
-                launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st, fwd_mode);
+                launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), piv_flags(), st, fwd_mode);
                 reghost_after_tma(nxt);
             }
             ev_mark("solve1");
@@ -867,7 +874,7 @@ struct Engine : EngineBase {
         case BSQ_PH_SOLVE1B:
             if (piped) {
                 ++step_launches;
-                launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), pos_pivots, st, SOLVE_YBWD);
+                launch_solve(C, solve_maps(1, nxt), solve_ptrs(nxt), piv_flags(), st, SOLVE_YBWD);
                 reghost_after_tma(nxt);
                 ev_mark("solve1b");
             }
@@ -885,14 +892,14 @@ struct Engine : EngineBase {
                 if (d.solver == BSQ_CR)
                     launch_cr(C, cr_ptrs(2, nxt), st);
                 else
-                    launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st, fwd_mode);
+                    launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), piv_flags(), st, fwd_mode);
                 ev_mark("solve2");
             }
             break;
         case BSQ_PH_SOLVE2B:
             if (d.cross_correction && piped) {
                 ++step_launches;
-                launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st, SOLVE_YBWD);
+                launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), piv_flags(), st, SOLVE_YBWD);
                 ev_mark("solve2b");
             }
             break;
@@ -1184,7 +1191,7 @@ struct Engine : EngineBase {
             CU(cudaMemsetAsync(&dres->cr_bad, 0xFF, sizeof(unsigned int), st));
             launch_cr(C, cr_ptrs(2, nxt), st);  // into P2 / Q2
         } else {
-            launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), pos_pivots, st);
+            launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), piv_flags(), st);
         }
         CU(cudaGetLastError());
         if ((rc = download_interior(pout, arr[A_P2])) || (rc = download_interior(qout, arr[A_Q2])))

@@ -89,8 +89,10 @@ size_t frame_elems(int nx, int ny);
 template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
                   cudaStream_t st);
+// pivot properties of a factored operator (launch_solve's `pivots`)
+enum { PIV_POSITIVE = 1, PIV_RDEN_INRANGE = 2 };
 template <class T>
-void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, bool pos_pivots,
+void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, int pivots,
                   cudaStream_t st, int mode = SOLVE_FULL);
 int solve_chunk_elems(int elem_bytes);
 template <class T>

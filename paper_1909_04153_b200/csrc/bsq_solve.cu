@@ -61,7 +61,10 @@ __device__ __forceinline__ int toff(int ln, int k) {
 // internal south side the first element continues the recurrence from dw_in
 // instead of folding a ghost; with an internal north side the last element
 // is not folded and the back substitution starts from x_in.
-template <class T, bool XDIR, bool POS>
+// RDEN_ONCHIP: RN(1/den) is recomputed in the consumer (3 streamed operands
+// instead of 4; 0.347 -> 0.310 ms per solve at 4096^2) whenever every pivot's
+// exponent is within +-1000 (PIV_RDEN_INRANGE, checked at factor time)
+template <class T, bool XDIR, bool POS, bool RDEN_ONCHIP>
 __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
                                 int line0, unsigned char *smem, int mode) {
     using G = TileGeom<T>;
@@ -106,14 +109,18 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
             for (int c = 0; c < nc; c++) {
                 const int s = c % NS;
                 if (c >= NS) mbar_wait(&empty[s], ((c / NS) - 1) & 1);
-                mbar_expect_tx(&full[s], 4 * G::TILE_B);
                 int c0, c1;
                 coords(c, c0, c1);
                 T *st = ring + s * 4 * TILE;
+                if (RDEN_ONCHIP) {
+                    mbar_expect_tx(&full[s], 3 * G::TILE_B);
+                } else {
+                    mbar_expect_tx(&full[s], 4 * G::TILE_B);
+                    tma_load_2d(st + 3 * TILE, m_rden, c0, c1, &full[s]);
+                }
                 tma_load_2d(st, m_rhs, c0, c1, &full[s]);
                 tma_load_2d(st + TILE, m_a, c0, c1, &full[s]);
                 tma_load_2d(st + 2 * TILE, m_den, c0, c1, &full[s]);
-                tma_load_2d(st + 3 * TILE, m_rden, c0, c1, &full[s]);
             }
         }
     } else {
@@ -129,9 +136,15 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                             : S.gq[L.at(GL - 1, GL + line)];
         const T g1 = (!lv || nint) ? T(0) : XDIR ? S.gp[L.at(GL + line, n + GL)] : S.gq[L.at(n + GL, GL + line)];
         const T cl = (!lv || nint) ? T(0) : XDIR ? S.cx_last[line] : S.cy_last[line];
-        // dw_i = (r_i - a_i dw_{i-1}) / den_i; the ring holds nr = -RN(1/den)
+        // dw_i = (r_i - a_i dw_{i-1}) / den_i with nr = -RN(1/den): streamed
+        // from HBM, or (RDEN_ONCHIP) recomputed here off the recurrence's
+        // critical path with the branch-free reciprocal (every pivot's exponent
+        // is within +-1000, checked at factor time)
         auto step = [&](T num, T den, T nr) -> T {
             return POS ? div_static_pos(num, den, nr) : div_static(num, den, -nr);
+        };
+        auto nrden = [&](const T *st, int t) -> T {
+            return RDEN_ONCHIP ? -rcp_rn_inrange(st[2 * TILE + t]) : st[3 * TILE + t];
         };
         T dw = T(0);
         for (int c = 0; c < nc; c++) {
@@ -153,7 +166,11 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                     rv[k] = st[t];
                     av[k] = st[TILE + t];
                     dv[k] = st[2 * TILE + t];
-                    nv[k] = st[3 * TILE + t];
+                    nv[k] = RDEN_ONCHIP ? T(0) : st[3 * TILE + t];
+                }
+                if (RDEN_ONCHIP) {
+#pragma unroll
+                    for (int k = 0; k < EK; k++) nv[k] = -rcp_rn_inrange(dv[k]);
                 }
 #pragma unroll
                 for (int k = 0; k < EK; k++) {
@@ -169,10 +186,10 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                     T r = st[t];
                     const T a = st[TILE + t];
                     if (e == 0) {  // folded, no recurrence term (thomas_batch dw[0])
-                        dw = step(r - a * g0, st[2 * TILE + t], st[3 * TILE + t]);
+                        dw = step(r - a * g0, st[2 * TILE + t], nrden(st, t));
                     } else {
                         if (e == n - 1) r = r - cl * g1;  // far ghost
-                        dw = step(r - a * dw, st[2 * TILE + t], st[3 * TILE + t]);
+                        dw = step(r - a * dw, st[2 * TILE + t], nrden(st, t));
                     }
                     ob[t] = dw;
                 }
@@ -266,44 +283,59 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
 }
 
 // Blocks [0, nbx) take x lines (rows -> P); blocks [nbx, ...) y lines (columns -> Q).
-template <class T, bool POS>
+template <class T, bool POS, bool ONCHIP>
 __global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_constant__ SolveMaps M,
                                                   SolvePtrs<T> S, int nbx, int mode) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     if ((int)blockIdx.x < nbx)
-        solve_lines_tma<T, true, POS>(C, M, S, blockIdx.x * NLINE, smem, mode);
+        solve_lines_tma<T, true, POS, ONCHIP>(C, M, S, blockIdx.x * NLINE, smem, mode);
     else
-        solve_lines_tma<T, false, POS>(C, M, S, (blockIdx.x - nbx) * NLINE, smem, mode);
+        solve_lines_tma<T, false, POS, ONCHIP>(C, M, S, (blockIdx.x - nbx) * NLINE, smem, mode);
 }
 
 // pos_pivots: every Thomas pivot of both operators is > 0 (host-checked), which
 // enables the select-free quotient on the recurrence's critical path.
 // mode SOLVE_YBWD launches only the y-line CTAs.
 template <class T>
-void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, bool pos_pivots,
+void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, int pivots,
                   cudaStream_t st, int mode) {
     const int nbx = (C.L.ny + NLINE - 1) / NLINE, nby = (C.L.nx + NLINE - 1) / NLINE;
     const int smem = TileGeom<T>::SMEM_B;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_solve_tma<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_solve_tma<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_solve_tma<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_solve_tma<T, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_solve_tma<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_solve_tma<T, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
     const int bx = mode == SOLVE_YBWD ? 0 : nbx;  // x-line CTAs in this launch
-    if (pos_pivots)
-        k_solve_tma<T, true><<<bx + nby, 64, smem, st>>>(C, M, S, bx, mode);
+    const bool pos = pivots & PIV_POSITIVE;
+#ifdef BSQ_SOLVE_RDEN_HBM
+    const bool onchip = false;
+#else
+    // fp32 keeps the streamed reciprocal: __frcp_rn's range branch serializes
+    // the consumer (0.19 -> 0.34 ms measured)
+    const bool onchip = sizeof(T) == 8 && (pivots & PIV_RDEN_INRANGE);
+#endif
+    dim3 g(bx + nby), b(64);
+    if (pos && onchip)
+        k_solve_tma<T, true, true><<<g, b, smem, st>>>(C, M, S, bx, mode);
+    else if (pos)
+        k_solve_tma<T, true, false><<<g, b, smem, st>>>(C, M, S, bx, mode);
+    else if (onchip)
+        k_solve_tma<T, false, true><<<g, b, smem, st>>>(C, M, S, bx, mode);
     else
-        k_solve_tma<T, false><<<bx + nby, 64, smem, st>>>(C, M, S, bx, mode);
+        k_solve_tma<T, false, false><<<g, b, smem, st>>>(C, M, S, bx, mode);
 }
 
 int solve_chunk_elems(int elem_bytes) { return 128 / elem_bytes; }
 
 template void launch_solve<double>(const Consts<double> &, const SolveMaps &,
-                                   const SolvePtrs<double> &, bool, cudaStream_t, int);
+                                   const SolvePtrs<double> &, int, cudaStream_t, int);
 template void launch_solve<float>(const Consts<float> &, const SolveMaps &,
-                                  const SolvePtrs<float> &, bool, cudaStream_t, int);
+                                  const SolvePtrs<float> &, int, cudaStream_t, int);
 
 }  // namespace bsq
