@@ -14,7 +14,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file $OUT/${TAG}_launches.csv python tools/profile_step.py --steps 2 \
     > $OUT/${TAG}_ncu_l.log 2>&1
 echo "launch list rc=$?"
-# skip the initial extrema + 3 warm-up steps (7 launches each): one AB3 step
-ncu --set full --clock-control none --import-source on -s 22 -c 7 \
-    -o $OUT/${TAG} -f python tools/profile_step.py --steps 1 > $OUT/${TAG}_ncu.log 2>&1
+# one AB3 step with speculation: skip the initial extrema, step 1 (ghost_t,
+# stage, ghost_n, solve1, correct, solve2, final + the queued frame, ghost_t,
+# stage = 10) and steps 2-3 (8 each), then capture step 4's 8 launches
+# (ghost_n .. final, and the queued frame, ghost_t, stage of step 5)
+ncu --set full --clock-control none --import-source on -s 27 -c 8 \
+    -o $OUT/${TAG} -f python tools/profile_step.py --steps 2 > $OUT/${TAG}_ncu.log 2>&1
 echo "full rc=$?"
