@@ -43,9 +43,9 @@ B_ALG_STEP = 424  # compulsory fp64 bytes per cell-update
 # algorithmic bytes per interior cell, per kernel launch
 KERNEL_BYTES = {
     "stage": 8 * 29,    # R w,P,Q + 6 static + 10 history; W 5 stages + w* + U*,V* + 2 bases
-    "solve1": 8 * 12,   # per direction: R rhs + 4 LU factors, W result
+    "solve1": 8 * 10,   # per direction: R rhs, a, den, cw (RN(1/den) on chip), W result
     "correct": 8 * 11,  # R base_u, base_v, F*_n, G*_n, P1, Q1, depth, d_x, d_y; W 2 RHS
-    "solve2": 8 * 12,
+    "solve2": 8 * 10,
     "final": 8 * 7,     # R w*, bed_eff, P2, Q2; W w, P, Q
 }
 
