@@ -516,9 +516,62 @@ struct Engine : EngineBase {
         return BSQ_OK;
     }
 
+    // TMA descriptor of a padded array (origin at padded cell (0, 0)), `cols`
+    // x `rows` cells, for `bc` x `br` boxes (the stage's tile loads)
+    int make_map_box(CUtensorMap *m, T *base, int cols, int rows, int bc, int br) {
+        auto encode = tensor_map_encoder();
+        if (!encode) return fail(BSQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+        cuuint64_t strides[1] = {(cuuint64_t)L.pitch * sizeof(T)};
+        cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = encode(m, F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                            2, base + L.xo, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(BSQ_ERR_CUDA, "cuTensorMapEncodeTiled (stage box) failed");
+        return BSQ_OK;
+    }
+
+    // stage tile boxes: 36 x 12 (32 x 8 tile + 2-cell halo; fp32 boxes are
+    // only built, the fp32 stage is the column walk)
+    CUtensorMap smap_w[3], smap_p[2], smap_q[2], smap_be, smap_dep, smap_bfx, smap_bfy;
+    int build_stage_maps() {
+        // fp64 only: the fp32 stage is the column walk, and fp32's padded
+        // origin (xo = 30 floats) is not 16-byte aligned as a map base must be
+        if (!F64) return BSQ_OK;
+        const int nxt = d.nx + 4, nyt = d.ny + 4, HX = 36, HY = 12, TY = 8, TX = 32;
+        int rc;
+        for (int k = 0; k < 3; k++)
+            if ((rc = make_map_box(&smap_w[k], arr[kW[k]], nxt, nyt, HX, HY))) return rc;
+        for (int k = 0; k < 2; k++)
+            if ((rc = make_map_box(&smap_p[k], Pp(k), nxt, nyt, HX, HY)) ||
+                (rc = make_map_box(&smap_q[k], Qq(k), nxt, nyt, HX, HY)))
+                return rc;
+        if ((rc = make_map_box(&smap_be, arr[A_BE], nxt, nyt, HX, HY)) ||
+            (rc = make_map_box(&smap_dep, arr[A_DEP], nxt, nyt, HX, HY)) ||
+            (rc = make_map_box(&smap_bfx, arr[A_BFX], nxt - 1, nyt, HX, TY)) ||
+            (rc = make_map_box(&smap_bfy, arr[A_BFY], nxt, nyt - 1, TX, TY + 3)))
+            return rc;
+        return BSQ_OK;
+    }
+    StageMaps stage_maps_for(const T *w, const T *p, const T *q) {
+        StageMaps M;
+        for (int k = 0; k < 3; k++)
+            if (arr[kW[k]] == w) M.w = smap_w[k];
+        M.p = Pp(0) == p ? smap_p[0] : smap_p[1];
+        M.q = Qq(0) == q ? smap_q[0] : smap_q[1];
+        M.be = smap_be;
+        M.dep = smap_dep;
+        M.bfx = smap_bfx;
+        M.bfy = smap_bfy;
+        return M;
+    }
+
     int build_maps() {
         SolveMaps &M = maps;
         int rc;
+        if ((rc = build_stage_maps())) return rc;
         if ((rc = make_map(&M.x_rhs, arr[A_US], true)) || (rc = make_map(&M.x_a, arr[A_AX], true)) ||
             (rc = make_map(&M.x_den, arr[A_DENX], true)) ||
             (rc = make_map(&M.x_rden, arr[A_RDENX], true)) ||
@@ -853,7 +906,8 @@ struct Engine : EngineBase {
         case BSQ_PH_STAGE:
             if (!spec_used) {
                 ++step_launches;
-                launch_stage(C, dparams, stage_ptrs(slot), 1, st);
+                const StageMaps sm = stage_maps_for(W(cur), Pp(cur), Qq(cur));
+                launch_stage(C, dparams, stage_ptrs(slot), 1, st, &sm);
                 fold_req = false;
                 ev_mark("stage");
             }
@@ -970,8 +1024,9 @@ struct Engine : EngineBase {
             launch_ghost(C, pn, 0, W(nxt), Pp(nxt), Qq(nxt), W(nxt), Pp(nxt), Qq(nxt), st);
             pre("ghost_t");
             ++step_launches;
+            const StageMaps sm = stage_maps_for(W(nxt), Pp(nxt), Qq(nxt));
             launch_stage(C, pn, stage_ptrs_on(W(nxt), Pp(nxt), Qq(nxt), (slot + 1) % 4, slot, head,
-                                              Wspare()), 1, st);
+                                              Wspare()), 1, st, &sm);
             pre("stage");
             CU(cudaGetLastError());
             spec_pending = true;
@@ -1161,7 +1216,8 @@ struct Engine : EngineBase {
         spec_pending = false;
         CU(cudaMemsetAsync(dres, 0xFF, sizeof(DevResult), st));
         const int slot = (head + 1) % 4;
-        launch_stage(C, dparams, stage_ptrs(slot), 0, st);
+        const StageMaps sm = stage_maps_for(W(cur), Pp(cur), Qq(cur));
+        launch_stage(C, dparams, stage_ptrs(slot), 0, st, &sm);
         fold_req = false;
         CU(cudaGetLastError());
         int rc;

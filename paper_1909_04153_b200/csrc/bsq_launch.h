@@ -83,12 +83,18 @@ struct FinalPtrs {
 template <class T>
 void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
                   const T *sq, T *dw, T *dp, T *dq, cudaStream_t st);
+// TMA descriptors of the stage tile loads (padded arrays; boxes of the
+// tile + 2-cell halo, 36 x 12 cells, and of the face beds)
+struct StageMaps {
+    CUtensorMap w, p, q, be, dep, bfx, bfy;
+};
+
 template <class T>
 void launch_frame(const Consts<T> &C, T *w, T *p, T *q, T *buf, int save, cudaStream_t st);
 size_t frame_elems(int nx, int ny);
 template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
-                  cudaStream_t st);
+                  cudaStream_t st, const StageMaps *M = nullptr);
 // pivot properties of a factored operator (launch_solve's `pivots`)
 enum { PIV_POSITIVE = 1, PIV_RDEN_INRANGE = 2 };
 template <class T>

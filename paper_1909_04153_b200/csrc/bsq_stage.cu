@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
 
 template <class T>
 void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
-                        cudaStream_t st);
+                        cudaStream_t st, const StageMaps *M);
 
 // fp64 runs the tiled variant (bsq_stage_tiled.cu: 64 registers, 32 warps per
 // SM, 1.31 ms at 4096^2) -- the column walk needs 128 fp64 registers and
@@ -349,9 +349,9 @@ void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<
 // registers; 1.50 vs 1.66 ms per step).  Measured A/B on B200, round 1.
 template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
-                  cudaStream_t st) {
+                  cudaStream_t st, const StageMaps *M) {
     if constexpr (sizeof(T) == 8) {
-        launch_stage_tiled(C, P, A, predict, st);
+        launch_stage_tiled(C, P, A, predict, st, M);
     } else {
         const size_t smem = sizeof(StageSmem<T>);
         static bool attr_set = false;
@@ -366,8 +366,8 @@ void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A,
 }
 
 template void launch_stage<double>(const Consts<double> &, const DevParams *,
-                                   const StagePtrs<double> &, int, cudaStream_t);
+                                   const StagePtrs<double> &, int, cudaStream_t, const StageMaps *);
 template void launch_stage<float>(const Consts<float> &, const DevParams *,
-                                  const StagePtrs<float> &, int, cudaStream_t);
+                                  const StagePtrs<float> &, int, cudaStream_t, const StageMaps *);
 
 }  // namespace bsq

@@ -24,6 +24,7 @@
 
 #include "bsq_device.cuh"
 #include "bsq_launch.h"
+#include "bsq_tma.cuh"
 
 namespace bsq {
 
@@ -43,11 +44,16 @@ constexpr int NXI = TY * (TX + 1), NYI = (TY + 1) * TX;  // interface items
 constexpr int NFL = NXI + NYI;
 constexpr int FL_PASSES = (NFL + NT - 1) / NT;
 
+// TMA boxes need 16-byte multiples along x: the bed_face_x box is HX wide
+// (one column more than used)
+constexpr int BFXW = HX;
+
 template <class T>
 struct StageSmem {
-    T w[HY][HX], p[HY][HX], q[HY][HX], eta[HY][HX];
-    T bfx[TY][TX + 3];  // bed_face_x for columns -2..TX
+    T w[HY][HX], p[HY][HX], q[HY][HX], be[HY][HX], dep[HY][HX], eta[HY][HX];
+    T bfx[TY][BFXW];    // bed_face_x for columns -2..TX
     T bfy[TY + 3][TX];  // bed_face_y for rows -2..TY
+    alignas(8) uint64_t bar;
     union {
         struct {  // phase B/C: faces (hi = east/north, lo = west/south)
             T xwhi[TY][FXW], xwlo[TY][FXW], xphi[TY][FXW], xplo[TY][FXW], xqhi[TY][FXW],
@@ -65,50 +71,34 @@ struct StageSmem {
 
 template <class T>
 __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const DevParams *__restrict__ P,
-                                                 StagePtrs<T> A, int predict) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+                                                 StagePtrs<T> A, int predict,
+                                                 const __grid_constant__ StageMaps M) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     StageSmem<T> &S = *reinterpret_cast<StageSmem<T> *>(smem_raw);
     const Layout L = C.L;
-    const int nx = L.nx, ny = L.ny, nxt = nx + 4, nyt = ny + 4;
+    const int nx = L.nx, ny = L.ny;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int I0 = GL + blockIdx.x * TX, J0 = GL + blockIdx.y * TY;
 
-    // ---- A: tile + halo ------------------------------------------------------
-    // Every global load of the phase is issued before the first shared store
-    // (fixed trip counts, unrolled), so the CTA pays one DRAM latency here
-    // instead of one per loop trip.
-    constexpr int PA = (HY * HX + NT - 1) / NT;
-    constexpr int PX = (TY * (TX + 3) + NT - 1) / NT;
-    constexpr int PY = ((TY + 3) * TX + NT - 1) / NT;
-    T lw[PA], lp[PA], lq[PA], lb[PA], ld[PA], lfx[PX], lfy[PY];
-#pragma unroll
-    for (int s = 0; s < PA; s++) {
-        const int k = tid + s * NT;
-        const int y = k / HX, x = k - y * HX;
-        const int J = J0 - 2 + y, I = I0 - 2 + x;
-        const bool in = k < HY * HX && J < nyt && I < nxt;
-        const long o = in ? L.at(J, I) : 0;
-        lw[s] = in ? A.w[o] : T(0);
-        lp[s] = in ? A.p[o] : T(0);
-        lq[s] = in ? A.q[o] : T(0);
-        lb[s] = in ? A.be[o] : T(0);
-        ld[s] = in ? A.dep[o] : T(0);
+    // ---- A: tile + halo, by TMA ------------------------------------------------
+    // One thread issues seven 2-D bulk tensor copies (w, P, Q, bed_eff, depth
+    // over the tile + 2-cell halo; the two face-bed boxes); out-of-grid cells
+    // arrive zero-filled, as the reference's padding needs none of them.
+    if (tid == 0) {
+        mbar_init(&S.bar, 1);
+        fence_mbar_init();
     }
-#pragma unroll
-    for (int s = 0; s < PX; s++) {
-        const int k = tid + s * NT;
-        const int y = k / (TX + 3), x = k - y * (TX + 3);
-        const int J = J0 + y, I = I0 - 2 + x;
-        const bool in = k < TY * (TX + 3) && J < nyt && I <= nx + 2;
-        lfx[s] = in ? A.bfx[L.at(J, I)] : T(0);
-    }
-#pragma unroll
-    for (int s = 0; s < PY; s++) {
-        const int k = tid + s * NT;
-        const int y = k / TX, x = k - y * TX;
-        const int J = J0 - 2 + y, I = I0 + x;
-        const bool in = k < (TY + 3) * TX && J <= ny + 2 && I < nxt;
-        lfy[s] = in ? A.bfy[L.at(J, I)] : T(0);
+    __syncthreads();
+    if (tid == 0) {
+        const int x0 = I0 - GL, y0 = J0 - GL;  // padded coordinates of the halo box
+        mbar_expect_tx(&S.bar, (unsigned)sizeof(T) * (5 * HY * HX + TY * BFXW + (TY + 3) * TX));
+        tma_load_2d(&S.w[0][0], &M.w, x0, y0, &S.bar);
+        tma_load_2d(&S.p[0][0], &M.p, x0, y0, &S.bar);
+        tma_load_2d(&S.q[0][0], &M.q, x0, y0, &S.bar);
+        tma_load_2d(&S.be[0][0], &M.be, x0, y0, &S.bar);
+        tma_load_2d(&S.dep[0][0], &M.dep, x0, y0, &S.bar);
+        tma_load_2d(&S.bfx[0][0], &M.bfx, x0, J0, &S.bar);
+        tma_load_2d(&S.bfy[0][0], &M.bfy, I0, y0, &S.bar);
     }
     // phase D's per-cell inputs that phase A does not read: start them towards
     // L2 now (no registers held), so phase D's loads hit on chip
@@ -128,32 +118,10 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
             }
         }
     }
-#pragma unroll
-    for (int s = 0; s < PA; s++) {
-        const int k = tid + s * NT;
-        if (k < HY * HX) {
-            const int y = k / HX, x = k - y * HX;
-            S.w[y][x] = lw[s];
-            S.p[y][x] = lp[s];
-            S.q[y][x] = lq[s];
-            S.eta[y][x] = (lw[s] - lb[s]) - ld[s];  // dispersion.py:87
-        }
-    }
-#pragma unroll
-    for (int s = 0; s < PX; s++) {
-        const int k = tid + s * NT;
-        if (k < TY * (TX + 3)) {
-            const int y = k / (TX + 3), x = k - y * (TX + 3);
-            S.bfx[y][x] = lfx[s];
-        }
-    }
-#pragma unroll
-    for (int s = 0; s < PY; s++) {
-        const int k = tid + s * NT;
-        if (k < (TY + 3) * TX) {
-            const int y = k / TX, x = k - y * TX;
-            S.bfy[y][x] = lfy[s];
-        }
+    mbar_wait(&S.bar, 0);
+    // eta = (w - bed_eff) - depth over the halo box (dispersion.py:87)
+    for (int k = tid; k < HY * HX; k += NT) {
+        (&S.eta[0][0])[k] = ((&S.w[0][0])[k] - (&S.be[0][0])[k]) - (&S.dep[0][0])[k];
     }
     __syncthreads();
 
@@ -246,7 +214,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
            (S.u.x.fy[0][ty + 1][tx] - S.u.x.fy[0][ty][tx]) * C.inv_dy;
     const T src_x = -C.g * (wc - T(0.5) * (be_ + bw_)) * (be_ - bw_) * C.inv_dx;
     const T src_y = -C.g * (wc - T(0.5) * (bn_ + bs_)) * (bn_ - bs_) * C.inv_dy;
-    T h = wc - A.be[o];
+    T h = wc - S.be[y][x];
     if (h < T(0)) h = T(0);
     const T hstar = h > C.h_eps ? h : C.h_eps;
     T fric = T(0);
@@ -256,7 +224,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     T rq = -(S.u.x.fx[2][ty][tx + 1] - S.u.x.fx[2][ty][tx]) * C.inv_dx -
            (S.u.x.fy[2][ty + 1][tx] - S.u.x.fy[2][ty][tx]) * C.inv_dy + src_y - fric * qc;
 
-    const T d = A.dep[o], dx_ = A.ddx[o], dy_ = A.ddy[o];
+    const T d = S.dep[y][x], dx_ = A.ddx[o], dy_ = A.ddy[o];
     T fs_, gs_;
     if (d > T(0)) {
         // dispersive_rates (_kernels.py:269-288)
@@ -353,7 +321,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
 
 template <class T>
 void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
-                        cudaStream_t st) {
+                        cudaStream_t st, const StageMaps *M) {
     const size_t smem = sizeof(tiled::StageSmem<T>);
     static bool attr_set = false;
     if (!attr_set) {
@@ -361,12 +329,14 @@ void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<
         attr_set = true;
     }
     dim3 grid((C.L.nx + tiled::TX - 1) / tiled::TX, (C.L.ny + tiled::TY - 1) / tiled::TY);
-    tiled::k_stage<T><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, A, predict);
+    tiled::k_stage<T><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, A, predict, *M);
 }
 
 template void launch_stage_tiled<double>(const Consts<double> &, const DevParams *,
-                                         const StagePtrs<double> &, int, cudaStream_t);
+                                         const StagePtrs<double> &, int, cudaStream_t,
+                                         const StageMaps *);
 template void launch_stage_tiled<float>(const Consts<float> &, const DevParams *,
-                                        const StagePtrs<float> &, int, cudaStream_t);
+                                        const StagePtrs<float> &, int, cudaStream_t,
+                                        const StageMaps *);
 
 }  // namespace bsq
