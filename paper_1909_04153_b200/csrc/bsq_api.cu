@@ -516,17 +516,19 @@ struct Engine : EngineBase {
         return BSQ_OK;
     }
 
-    // TMA descriptor of a padded array (origin at padded cell (0, 0)), `cols`
-    // x `rows` cells, for `bc` x `br` boxes (the stage's tile loads)
+    // TMA descriptor of a padded array for `bc` x `br` boxes (the stage's tile
+    // loads).  The map starts at the pitched row start (128-B aligned, as a
+    // map base must be 16-B aligned and fp32's padded origin xo = 30 is not):
+    // box x coordinates carry + xo, and `cols` padded columns follow xo.
     int make_map_box(CUtensorMap *m, T *base, int cols, int rows, int bc, int br) {
         auto encode = tensor_map_encoder();
         if (!encode) return fail(BSQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+        cuuint64_t dims[2] = {(cuuint64_t)(L.xo + cols), (cuuint64_t)rows};
         cuuint64_t strides[1] = {(cuuint64_t)L.pitch * sizeof(T)};
         cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
         cuuint32_t estr[2] = {1, 1};
         CUresult r = encode(m, F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                            2, base + L.xo, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(BSQ_ERR_CUDA, "cuTensorMapEncodeTiled (stage box) failed");
@@ -537,9 +539,6 @@ struct Engine : EngineBase {
     // only built, the fp32 stage is the column walk)
     CUtensorMap smap_w[3], smap_p[2], smap_q[2], smap_be, smap_dep, smap_bfx, smap_bfy;
     int build_stage_maps() {
-        // fp64 only: the fp32 stage is the column walk, and fp32's padded
-        // origin (xo = 30 floats) is not 16-byte aligned as a map base must be
-        if (!F64) return BSQ_OK;
         const int nxt = d.nx + 4, nyt = d.ny + 4, HX = 36, HY = 12, TY = 8, TX = 32;
         int rc;
         for (int k = 0; k < 3; k++)

@@ -50,9 +50,15 @@ constexpr int BFXW = HX;
 
 template <class T>
 struct StageSmem {
-    T w[HY][HX], p[HY][HX], q[HY][HX], be[HY][HX], dep[HY][HX], eta[HY][HX];
-    T bfx[TY][BFXW];    // bed_face_x for columns -2..TX
-    T bfy[TY + 3][TX];  // bed_face_y for rows -2..TY
+    // TMA destinations: 128-byte aligned each
+    alignas(128) T w[HY][HX];
+    alignas(128) T p[HY][HX];
+    alignas(128) T q[HY][HX];
+    alignas(128) T be[HY][HX];
+    alignas(128) T dep[HY][HX];
+    alignas(128) T eta[HY][HX];
+    alignas(128) T bfx[TY][BFXW];    // bed_face_x for columns -2..TX
+    alignas(128) T bfy[TY + 3][TX];  // bed_face_y for rows -2..TY
     alignas(8) uint64_t bar;
     union {
         struct {  // phase B/C: faces (hi = east/north, lo = west/south)
@@ -73,8 +79,11 @@ template <class T>
 __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const DevParams *__restrict__ P,
                                                  StagePtrs<T> A, int predict,
                                                  const __grid_constant__ StageMaps M) {
+    // the TMA destinations need 128-B alignment: the kernel has no static
+    // smem, so the dynamic window starts at the CTA's smem base (checked)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     StageSmem<T> &S = *reinterpret_cast<StageSmem<T> *>(smem_raw);
+    if (threadIdx.x == 0 && threadIdx.y == 0 && (smem_u32(smem_raw) & 127u) != 0) __trap();
     const Layout L = C.L;
     const int nx = L.nx, ny = L.ny;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
@@ -90,7 +99,9 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     }
     __syncthreads();
     if (tid == 0) {
-        const int x0 = I0 - GL, y0 = J0 - GL;  // padded coordinates of the halo box
+        // halo box origin: padded column I0 - 2 (+ xo: the maps start at the
+        // pitched row), padded row J0 - 2
+        const int x0 = L.xo + I0 - GL, y0 = J0 - GL;
         mbar_expect_tx(&S.bar, (unsigned)sizeof(T) * (5 * HY * HX + TY * BFXW + (TY + 3) * TX));
         tma_load_2d(&S.w[0][0], &M.w, x0, y0, &S.bar);
         tma_load_2d(&S.p[0][0], &M.p, x0, y0, &S.bar);
@@ -98,7 +109,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         tma_load_2d(&S.be[0][0], &M.be, x0, y0, &S.bar);
         tma_load_2d(&S.dep[0][0], &M.dep, x0, y0, &S.bar);
         tma_load_2d(&S.bfx[0][0], &M.bfx, x0, J0, &S.bar);
-        tma_load_2d(&S.bfy[0][0], &M.bfy, I0, y0, &S.bar);
+        tma_load_2d(&S.bfy[0][0], &M.bfy, L.xo + I0, y0, &S.bar);
     }
     // phase D's per-cell inputs that phase A does not read: start them towards
     // L2 now (no registers held), so phase D's loads hit on chip
