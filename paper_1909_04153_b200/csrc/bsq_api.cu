@@ -490,7 +490,7 @@ struct Engine : EngineBase {
     int spike_fix(int solve, const void *ybound) {
         if (!d_sptab) return fail(BSQ_ERR_BAD_ARG, "spike table not set");
         if ((solve != 1 && solve != 2) || !ybound) return fail(BSQ_ERR_BAD_ARG, "bad spike_fix args");
-        T *x = solve == 1 ? Qq(1 - cur) : arr[A_Q2];
+        T *x = Qq(1 - cur);  // both solves land in the pending Q
         T *bt = (T *)(base + offs[A_COUNT + S_SPBT]);
         launch_spike(C, sp_G, sp_rank, d_sptab, (const T *)ybound, bt, x, arr[A_SPV], arr[A_SPW],
                      d.south_internal, d.north_internal, st);
@@ -808,8 +808,11 @@ struct Engine : EngineBase {
 
     // phase 1 solves U*, V* into the pending state's P, Q; phase 2 solves the
     // corrected right-hand sides (written over us / vs) into P2, Q2
-    const SolveMaps &solve_maps(int phase, int nxt_state) {
-        const int k = phase == 1 ? nxt_state : 2;
+    // Both solves write the pending state's P, Q (the second overwrites the
+    // first once the cross terms have read it); `scratch` sends a second solve
+    // to P2 / Q2 instead (the bsq_solve_momentum seam)
+    const SolveMaps &solve_maps(int phase, int nxt_state, bool scratch = false) {
+        const int k = (phase == 2 && scratch) ? 2 : nxt_state;
         maps.x_out = map_xout[k];
         maps.y_out = map_yout[k];
         return maps;
@@ -944,8 +947,10 @@ struct Engine : EngineBase {
                 ++step_launches;
                 if (d.solver == BSQ_CR)
                     launch_cr(C, cr_ptrs(2, nxt), st);
-                else
+                else {
                     launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), piv_flags(), st, fwd_mode);
+                    reghost_after_tma(nxt);
+                }
                 ev_mark("solve2");
             }
             break;
@@ -953,6 +958,7 @@ struct Engine : EngineBase {
             if (d.cross_correction && piped) {
                 ++step_launches;
                 launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), piv_flags(), st, SOLVE_YBWD);
+                reghost_after_tma(nxt);
                 ev_mark("solve2b");
             }
             break;
@@ -976,8 +982,8 @@ struct Engine : EngineBase {
     int finish(bsq_step_result *r, int slot, int nxt) {
         FinalPtrs<T> F;
         F.w = W(nxt);
-        F.pin = d.cross_correction ? arr[A_P2] : Pp(nxt);
-        F.qin = d.cross_correction ? arr[A_Q2] : Qq(nxt);
+        F.pin = Pp(nxt);  // the last solve's result, in place
+        F.qin = Qq(nxt);
         F.pout = Pp(nxt);
         F.qout = Qq(nxt);
         F.be = arr[A_BE];
@@ -1061,7 +1067,7 @@ struct Engine : EngineBase {
         return msg[(key & 3u) < 3u ? (key & 3u) : 0];
     }
 
-    CrPtrs<T> cr_ptrs(int phase, int nxt_state) {
+    CrPtrs<T> cr_ptrs(int phase, int nxt_state, bool scratch = false) {
         CrPtrs<T> K;
         K.ax = arr[A_AX];
         K.bx = arr[A_BX];
@@ -1073,8 +1079,8 @@ struct Engine : EngineBase {
         K.ry = arr[A_VS];
         K.gp = Pp(nxt_state);
         K.gq = Qq(nxt_state);
-        K.outx = phase == 1 ? Pp(nxt_state) : arr[A_P2];
-        K.outy = phase == 1 ? Qq(nxt_state) : arr[A_Q2];
+        K.outx = (phase == 2 && scratch) ? arr[A_P2] : Pp(nxt_state);
+        K.outy = (phase == 2 && scratch) ? arr[A_Q2] : Qq(nxt_state);
         K.bad = &dres->cr_bad;
         K.key_base = phase == 1 ? 0u : 1u << 31;
         return K;
@@ -1244,9 +1250,9 @@ struct Engine : EngineBase {
             return rc;
         if (d.solver == BSQ_CR) {
             CU(cudaMemsetAsync(&dres->cr_bad, 0xFF, sizeof(unsigned int), st));
-            launch_cr(C, cr_ptrs(2, nxt), st);  // into P2 / Q2
+            launch_cr(C, cr_ptrs(2, nxt, true), st);  // into P2 / Q2
         } else {
-            launch_solve(C, solve_maps(2, nxt), solve_ptrs(nxt), piv_flags(), st);
+            launch_solve(C, solve_maps(2, nxt, true), solve_ptrs(nxt), piv_flags(), st);
         }
         CU(cudaGetLastError());
         if ((rc = download_interior(pout, arr[A_P2])) || (rc = download_interior(qout, arr[A_Q2])))

@@ -151,6 +151,11 @@ __device__ void spec_next(const DevParams &P, double max_rate, DevParams &N, Spe
     o.wc = w0, o.wp = w1, o.wp2 = w2, o.sc = s0, o.sp = s1, o.sp2 = s2;
 }
 
+__device__ __forceinline__ unsigned long long bits(double v) {
+    return (unsigned long long)__double_as_longlong(v);
+}
+__device__ __forceinline__ unsigned long long bits(float v) { return __float_as_uint(v); }
+
 template <class T>
 __global__ void __launch_bounds__(FT) k_final(Consts<T> C, FinalPtrs<T> F) {
     __shared__ bool am_last;
@@ -200,9 +205,12 @@ __global__ void __launch_bounds__(FT) k_final(Consts<T> C, FinalPtrs<T> F) {
             p = p * fac;
             q = q * fac;
         }
-        F.w[o] = w;
-        F.pout[o] = p;
-        F.qout[o] = q;
+        // the solves left P, Q in place and w* is already the pending w: store
+        // only what the clamp, film cutoff or sponge changed (bit patterns
+        // compared, so a zero's sign is kept exactly)
+        if (bits(w) != bits(vw[k])) F.w[o] = w;
+        if (F.pout != F.pin || bits(p) != bits(vp[k])) F.pout[o] = p;
+        if (F.qout != F.qin || bits(q) != bits(vq[k])) F.qout[o] = q;
         T dv = w - rest;  // blow-up deviation (stepper.py:295)
         dv = dv < T(0) ? -dv : dv;
         if (dv != dv) r.nan = 1;

@@ -544,8 +544,7 @@ class ShardedDevice:
             self.strips[r].phase(ph_f)
         if solve == 2 and not self.cross:
             return
-        yb = self.comm.spike_bounds(self.strips, nat.ARR_Q_NEW if solve == 1 else nat.ARR_Q2,
-                                    self.stream)
+        yb = self.comm.spike_bounds(self.strips, nat.ARR_Q_NEW, self.stream)
         for r, s in self.strips.items():
             s.spike_fix(solve, yb[r])
 
