@@ -371,8 +371,9 @@ struct Engine : EngineBase {
             CW[o] = T(cw);
             if (!(dT > T(0))) pos = false;
             if (den == 0.0) sing = true;
-            const double ad = std::fabs(double(dT));  // rcp_rn_inrange's domain
-            if (!(ad >= 0x1p-1000 && ad <= 0x1p1000)) inrange = false;
+            // rcp_rn_inrange's verified domain: |exponent| <= 1000 (fp64), 100 (fp32)
+            const double ad = std::fabs(double(dT)), lim = F64 ? 0x1p1000 : 0x1p100;
+            if (!(ad >= 1.0 / lim && ad <= lim)) inrange = false;
         };
         for (int j = 0; j < ny; j++) {  // x rows
             double cw_prev = 0.0;

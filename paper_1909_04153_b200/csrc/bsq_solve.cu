@@ -316,9 +316,7 @@ void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
 #ifdef BSQ_SOLVE_RDEN_HBM
     const bool onchip = false;
 #else
-    // fp32 keeps the streamed reciprocal: __frcp_rn's range branch serializes
-    // the consumer (0.19 -> 0.34 ms measured)
-    const bool onchip = sizeof(T) == 8 && (pivots & PIV_RDEN_INRANGE);
+    const bool onchip = pivots & PIV_RDEN_INRANGE;
 #endif
     dim3 g(bx + nby), b(64);
     if (pos && onchip)
