@@ -274,24 +274,28 @@ def main():
     for _ in range(max(args.warmup, 3)):
         sim.advance()
     stream = sim._dev.stream
-    sim._dev.set_timing(True)
-    per_kernel = {}
     barrier()
     t_c0 = time.perf_counter()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)
     for _ in range(args.steps):
         sim.advance()
-        for name, ms in sim._dev.kernel_times():
-            per_kernel.setdefault(name, []).append(ms)
     end.record(stream)
     torch.cuda.synchronize(dev)
     t_c1 = time.perf_counter()
     ms_total = max_over_ranks(start.elapsed_time(end))
-    sim._dev.set_timing(False)
     ms_step = ms_total / args.steps
     value = cells_total * args.steps / (ms_total * 1e-3) / 1e9
     kps = sim._dev.kernels_per_step()
+    # per-kernel device times: the same steps again with CUDA events around
+    # every kernel (kept out of the timed region above)
+    sim._dev.set_timing(True)
+    per_kernel = {}
+    for _ in range(max(args.steps, 10)):
+        sim.advance()
+        for name, ms in sim._dev.kernel_times():
+            per_kernel.setdefault(name, []).append(ms)
+    sim._dev.set_timing(False)
     sim.close()
     del sim
     torch.cuda.empty_cache()
