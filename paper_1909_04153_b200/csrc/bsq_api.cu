@@ -540,7 +540,8 @@ struct Engine : EngineBase {
     // only built, the fp32 stage is the column walk)
     CUtensorMap smap_w[3], smap_p[2], smap_q[2], smap_be, smap_dep, smap_bfx, smap_bfy;
     int build_stage_maps() {
-        const int nxt = d.nx + 4, nyt = d.ny + 4, HX = 36, HY = 12, TY = 8, TX = 32;
+        const int nxt = d.nx + 4, nyt = d.ny + 4, TX = STAGE_TX, TY = STAGE_TY, HX = TX + 4,
+                  HY = TY + 4;
         int rc;
         for (int k = 0; k < 3; k++)
             if ((rc = make_map_box(&smap_w[k], arr[kW[k]], nxt, nyt, HX, HY))) return rc;

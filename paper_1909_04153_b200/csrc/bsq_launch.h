@@ -83,8 +83,14 @@ struct FinalPtrs {
 template <class T>
 void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
                   const T *sq, T *dw, T *dp, T *dq, cudaStream_t st);
+// stage tile (fp64 tiled kernel): STAGE_TX x STAGE_TY cells per CTA
+#ifndef BSQ_STAGE_TY
+#define BSQ_STAGE_TY 8
+#endif
+constexpr int STAGE_TX = 32, STAGE_TY = BSQ_STAGE_TY;
+
 // TMA descriptors of the stage tile loads (padded arrays; boxes of the
-// tile + 2-cell halo, 36 x 12 cells, and of the face beds)
+// tile + 2-cell halo, (TX+4) x (TY+4) cells, and of the face beds)
 struct StageMaps {
     CUtensorMap w, p, q, be, dep, bfx, bfy;
 };

@@ -33,10 +33,7 @@ namespace bsq {
 #endif
 
 namespace tiled {
-#ifndef BSQ_STAGE_TY
-#define BSQ_STAGE_TY 8
-#endif
-constexpr int TX = 32, TY = BSQ_STAGE_TY, NT = TX * TY;
+constexpr int TX = STAGE_TX, TY = STAGE_TY, NT = TX * TY;
 constexpr int HX = TX + 4, HY = TY + 4;       // tile + 2-cell halo
 constexpr int FXW = TX + 2, FYH = TY + 2;     // cells with x faces per row / rows with y faces
 constexpr int NXF = TY * FXW, NYF = FYH * TX; // face items
