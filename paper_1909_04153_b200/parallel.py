@@ -234,29 +234,38 @@ class DistComm:
                 d.send(s.vector(nat.ARR_X_OUT), r - 1, group=self.group)
 
     def reduce(self, parts: list, nx: int, rows0: list):
+        """One all_gather per step: every rank's reductions (maxima, NaN flag as
+        NaN, clamped volume, global first-bad indices) packed into 14
+        doubles, folded on every rank in rank order like LocalComm."""
         mine = _combine(parts, nx, rows0)
-        d, dev = self.dist, self._dev()
-        mx = torch.tensor([mine["max_rate"], mine["max_speed"], mine["max_depth"],
-                           -1.0 if math.isnan(mine["max_dev"]) else mine["max_dev"]],
-                          dtype=torch.float64, device=dev)
-        nan = torch.tensor([1 if math.isnan(mine["max_dev"]) else 0], dtype=torch.int64, device=dev)
-        big = np.iinfo(np.int64).max
-        bad = torch.tensor([b if b >= 0 else big for b in mine["stage_bad"] + mine["state_bad"]],
-                           dtype=torch.int64, device=dev)
-        cl = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(self.world)]
-        d.all_reduce(mx, op=d.ReduceOp.MAX, group=self.group)
-        d.all_reduce(nan, op=d.ReduceOp.MAX, group=self.group)
-        d.all_reduce(bad, op=d.ReduceOp.MIN, group=self.group)
-        d.all_gather(cl, torch.tensor([mine["clamped"]], dtype=torch.float64, device=dev),
-                     group=self.group)
-        m = mx.cpu().numpy()
-        bads = [int(b) if b != big else -1 for b in bad.cpu().numpy()]
-        clamped = 0.0
-        for c in cl:  # rank order: deterministic
-            clamped += float(c.item())
-        return {"max_rate": float(m[0]), "max_speed": float(m[1]), "max_depth": float(m[2]),
-                "max_dev": math.nan if nan.item() else float(m[3]), "clamped": clamped,
-                "stage_bad": bads[:5], "state_bad": bads[5:]}
+        vec = torch.tensor([mine["max_rate"], mine["max_speed"], mine["max_depth"],
+                            mine["max_dev"], mine["clamped"]]
+                           + [float(b) for b in mine["stage_bad"] + mine["state_bad"]],
+                           dtype=torch.float64, device=self._dev())
+        bufs = [torch.empty_like(vec) for _ in range(self.world)]
+        self.dist.all_gather(bufs, vec, group=self.group)
+        rows = torch.stack(bufs).cpu().numpy()
+        out = {"max_rate": 0.0, "max_speed": 0.0, "max_depth": 0.0, "max_dev": 0.0,
+               "clamped": 0.0, "stage_bad": [-1] * 5, "state_bad": [-1] * 3}
+        nan = False
+        for r in rows:  # rank order: the clamped sum is deterministic
+            out["max_rate"] = max(out["max_rate"], float(r[0]))
+            out["max_speed"] = max(out["max_speed"], float(r[1]))
+            out["max_depth"] = max(out["max_depth"], float(r[2]))
+            if math.isnan(r[3]):
+                nan = True
+            else:
+                out["max_dev"] = max(out["max_dev"], float(r[3]))
+            out["clamped"] += float(r[4])
+            for i, key, k in [(5 + j, "stage_bad", j) for j in range(5)] + \
+                    [(10 + j, "state_bad", j) for j in range(3)]:
+                g = int(r[i])
+                if g >= 0:
+                    cur = out[key][k]
+                    out[key][k] = g if cur < 0 else min(cur, g)
+        if nan:
+            out["max_dev"] = math.nan
+        return out
 
     def gather_state(self, locals_: dict, shape, ranges):
         (w, p, q), = locals_.values()
