@@ -78,9 +78,13 @@ void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st
     k_correct<T><<<grid, dim3(32, 8), 0, st>>>(C, K);
 }
 
+#if BSQ_INST_F64
 template void launch_correct<double>(const Consts<double> &, const CorrectPtrs<double> &,
                                      cudaStream_t);
+#endif
+#if BSQ_INST_F32
 template void launch_correct<float>(const Consts<float> &, const CorrectPtrs<float> &,
                                     cudaStream_t);
+#endif
 
 }  // namespace bsq

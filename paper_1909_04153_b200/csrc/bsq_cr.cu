@@ -131,10 +131,12 @@ static int pow2_at_least(int n) {
     return n2 < 2 ? 2 : n2;
 }
 
+#if BSQ_INST_F64
 size_t cr_smem_bytes(int nx, int ny, int elem) {
     const int n2 = pow2_at_least(nx > ny ? nx : ny);
     return (size_t)5 * n2 * elem;
 }
+#endif
 
 template <class T>
 void launch_cr(const Consts<T> &C, const CrPtrs<T> &K, cudaStream_t st) {
@@ -144,7 +146,11 @@ void launch_cr(const Consts<T> &C, const CrPtrs<T> &K, cudaStream_t st) {
     k_cr<T><<<C.L.ny + C.L.nx, CR_THREADS, smem, st>>>(C, K, C.L.ny, n2x, n2y);
 }
 
+#if BSQ_INST_F64
 template void launch_cr<double>(const Consts<double> &, const CrPtrs<double> &, cudaStream_t);
+#endif
+#if BSQ_INST_F32
 template void launch_cr<float>(const Consts<float> &, const CrPtrs<float> &, cudaStream_t);
+#endif
 
 }  // namespace bsq

@@ -16,31 +16,88 @@
 
 namespace bsq {
 
-constexpr int FX = 32, FY = 8, FR = 4;  // block 32 x 8 threads, 4 rows per thread
+__device__ __forceinline__ unsigned long long bits(double v) {
+    return (unsigned long long)__double_as_longlong(v);
+}
+__device__ __forceinline__ unsigned long long bits(float v) { return __float_as_uint(v); }
+__device__ __forceinline__ bool bits_nonzero(double v) { return bits(v) != 0ull; }
+
+#ifndef BSQ_FINAL_FR
+#define BSQ_FINAL_FR 8
+#endif
+#ifndef BSQ_FINAL_FG
+#define BSQ_FINAL_FG 4
+#endif
+constexpr int FX = 32, FY = 8, FR = BSQ_FINAL_FR;  // block 32 x 8 threads, FR rows per thread
+constexpr int FG = BSQ_FINAL_FG;  // rows loaded per batch (all loads first, then the work)
 constexpr int FT = FX * FY, FWARPS = FT / 32;
+#ifndef BSQ_FINAL_MINB
+#define BSQ_FINAL_MINB 4
+#endif
 
 struct Red {
     double rate, speed, depth, dev, clamp;
     int nan;
 };
 
-__device__ __forceinline__ void red_warp(Red &r) {
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) {
-        r.rate = fmax(r.rate, __shfl_xor_sync(0xffffffffu, r.rate, m));
-        r.speed = fmax(r.speed, __shfl_xor_sync(0xffffffffu, r.speed, m));
-        r.depth = fmax(r.depth, __shfl_xor_sync(0xffffffffu, r.depth, m));
-        r.dev = fmax(r.dev, __shfl_xor_sync(0xffffffffu, r.dev, m));
-        r.clamp = r.clamp + __shfl_xor_sync(0xffffffffu, r.clamp, m);
-        r.nan |= __shfl_xor_sync(0xffffffffu, r.nan, m);
-    }
+// per-thread accumulators in the kernel's precision: max is exact and the
+// conversion to double monotone, so the maxima equal the fp64-accumulated ones
+template <class T>
+struct Acc {
+    T rate, speed, depth, dev;
+    double clamp;
+    int nan;
+};
+
+// Warp max of non-negative, non-NaN values (the accumulators only ever take a
+// value strictly greater than +0 or keep +0): their bit patterns order like
+// the values, so redux.sync on the words does it -- high words first, then
+// the low words of the lanes holding the top high word.
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    return __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+}
+__device__ __forceinline__ float warp_max_nonneg(float v) {
+    return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(v)));
 }
 
-// CTA-wide reduction; result valid in thread 0
-__device__ __forceinline__ Red red_block(Red r) {
+// fixed-shape xor tree for the clamped-volume sum; skipped (+0) when the
+// whole warp has nothing to add
+__device__ __forceinline__ double warp_sum(double v) {
+    if (!__any_sync(0xffffffffu, bits_nonzero(v))) return v;
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, m);
+    return v;
+}
+
+__device__ __forceinline__ void red_warp(Red &r) {
+    r.rate = warp_max_nonneg(r.rate);
+    r.speed = warp_max_nonneg(r.speed);
+    r.depth = warp_max_nonneg(r.depth);
+    r.dev = warp_max_nonneg(r.dev);
+    r.clamp = warp_sum(r.clamp);
+    r.nan = __any_sync(0xffffffffu, r.nan);
+}
+
+template <class T>
+__device__ __forceinline__ Red red_warp(const Acc<T> &a) {
+    Red r;
+    r.rate = double(warp_max_nonneg(a.rate));
+    r.speed = double(warp_max_nonneg(a.speed));
+    r.depth = double(warp_max_nonneg(a.depth));
+    r.dev = double(warp_max_nonneg(a.dev));
+    r.clamp = warp_sum(a.clamp);
+    r.nan = __any_sync(0xffffffffu, a.nan);
+    return r;
+}
+
+// CTA-wide reduction of warp-reduced values; result valid in thread 0
+__device__ __forceinline__ Red red_block_warped(Red r) {
     __shared__ Red s[FWARPS];
     const int tid = threadIdx.y * FX + threadIdx.x;
-    red_warp(r);
     __syncthreads();  // protect s against a previous use
     if ((tid & 31) == 0) s[tid >> 5] = r;
     __syncthreads();
@@ -59,10 +116,18 @@ __device__ __forceinline__ Red red_block(Red r) {
     return r;
 }
 
+__device__ __forceinline__ Red red_block(Red r) {
+    red_warp(r);
+    return red_block_warped(r);
+}
+
 // speed_extrema contribution of one cell (_kernels.py:337-352); the serial
 // scan's `if x > max` skips NaN, hence the !(x > 0) guards.
 template <class T>
-__device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, T be, Red &r) {
+__device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, T be, Acc<T> &r) {
+    // a dry, still cell (h = 0, P = Q = 0) contributes rate = speed = depth = 0,
+    // which never raises a maximum: skip it (whole dry warps branch over)
+    if (!(w - be > T(0)) && p == T(0) && q == T(0)) return;
     T h = w - be;
     if (h < T(0)) h = T(0);
     const T hstar = h > C.h_eps ? h : C.h_eps;
@@ -70,11 +135,11 @@ __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, 
     const T nrh = -rcp_rn(hstar);  // both quotients correctly rounded via one reciprocal
     const T su = div_nonneg(fabs(p), hstar, nrh) + c;
     const T sv = div_nonneg(fabs(q), hstar, nrh) + c;
-    const double rate = double(nb_max(su * C.inv_dx, sv * C.inv_dy));
-    const double speed = double(nb_max(su, sv));
+    const T rate = nb_max(su * C.inv_dx, sv * C.inv_dy);
+    const T speed = nb_max(su, sv);
     if (rate > r.rate) r.rate = rate;
     if (speed > r.speed) r.speed = speed;
-    if (double(h) > r.depth) r.depth = double(h);
+    if (h > r.depth) r.depth = h;
 }
 
 // Python's min / max of two floats: the first argument unless the second is
@@ -88,7 +153,7 @@ __device__ __forceinline__ double py_max(double a, double b) { return b > a ? b 
 // vfd_weights, increment_weights), same operations in the same order.  The
 // host recomputes all of it and only uses the speculated stage if every
 // value agrees bit for bit.
-__device__ void spec_next(const DevParams &P, double max_rate, DevParams &N, SpecNext &o) {
+static __device__ void spec_next(const DevParams &P, double max_rate, DevParams &N, SpecNext &o) {
     double dt;
     if (P.adaptive) {
         const double cand = max_rate <= 0.0
@@ -151,89 +216,91 @@ __device__ void spec_next(const DevParams &P, double max_rate, DevParams &N, Spe
     o.wc = w0, o.wp = w1, o.wp2 = w2, o.sc = s0, o.sp = s1, o.sp2 = s2;
 }
 
-__device__ __forceinline__ unsigned long long bits(double v) {
-    return (unsigned long long)__double_as_longlong(v);
-}
-__device__ __forceinline__ unsigned long long bits(float v) { return __float_as_uint(v); }
 
 template <class T>
-__global__ void __launch_bounds__(FT) k_final(Consts<T> C, FinalPtrs<T> F) {
+__global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, FinalPtrs<T> F) {
     __shared__ bool am_last;
     const Layout L = C.L;
     const int nx = L.nx, ny = L.ny;
     const int I = GL + blockIdx.x * FX + threadIdx.x;
-    Red r{0, 0, 0, 0, 0, 0};
-    // all loads of the thread's cells first (pure stream), then the work
-    T vbe[FR], vw[FR], vp[FR], vq[FR];
+    const int J0 = GL + blockIdx.y * FR * FY + threadIdx.y;
+    const long rstep = (long)FY * L.pitch;
+    const long o0 = L.at(J0, I);
+    const bool iin = I < nx + GL;
+    Acc<T> r{T(0), T(0), T(0), T(0), 0.0, 0};
 #pragma unroll
-    for (int k = 0; k < FR; k++) {
-        const int J = GL + (blockIdx.y * FR + k) * FY + threadIdx.y;
-        const bool in = I < nx + GL && J < ny + GL;
-        const long o = in ? L.at(J, I) : L.at(GL, GL);
-        vbe[k] = F.be[o];
-        vw[k] = F.w[o];
-        vp[k] = F.pin[o];
-        vq[k] = F.qin[o];
+    for (int k0 = 0; k0 < FR; k0 += FG) {
+        // all loads of the batch first (pure stream), then the work
+        T vbe[FG], vw[FG], vp[FG], vq[FG];
+#pragma unroll
+        for (int k = 0; k < FG; k++) {
+            const bool in = iin && J0 + (k0 + k) * FY < ny + GL;
+            const long o = in ? o0 + (k0 + k) * rstep : L.at(GL, GL);
+            vbe[k] = F.be[o];
+            vw[k] = F.w[o];
+            vp[k] = F.pin[o];
+            vq[k] = F.qin[o];
+        }
+#pragma unroll
+        for (int k = 0; k < FG; k++) {
+            const int J = J0 + (k0 + k) * FY;
+            if (!iin || J >= ny + GL) continue;
+            const long o = o0 + (k0 + k) * rstep;
+            const T be = vbe[k];
+            T w = vw[k];
+            T p = vp[k], q = vq[k];
+            // clamp and volume tally (stepper.py:281-285); np.maximum keeps NaN
+            const T def = be - w;
+            if (def > T(0) || def != def) r.clamp = r.clamp + double(def);
+            w = (w >= be || w != w) ? w : be;
+            // film cutoff (stepper.py:288-292)
+            if (C.h_dry > T(0) && (w - be) < C.h_dry) {
+                p = T(0);
+                q = T(0);
+            }
+            const T rest = C.ws > be ? C.ws : be;  // np.maximum(ws, bed_eff)
+#pragma unroll
+            for (int side = 0; side < 4; side++) {  // sponge bands, order N, S, E, W
+                // band in local coordinates (a strip may hold part of a N/S band)
+                if (C.sponge_len[side] == 0) continue;
+                const int kk = (side == SIDE_E || side == SIDE_W) ? (I - GL) - C.sponge_lo[side]
+                                                                  : (J - GL) - C.sponge_lo[side];
+                if (kk < 0 || kk >= C.sponge_len[side]) continue;
+                const T fac = F.fac[side][kk];
+                w = rest + (w - rest) * fac;
+                p = p * fac;
+                q = q * fac;
+            }
+            // the solves left P, Q in place and w* is already the pending w: store
+            // only what the clamp, film cutoff or sponge changed (bit patterns
+            // compared, so a zero's sign is kept exactly)
+            if (bits(w) != bits(vw[k])) F.w[o] = w;
+            if (F.pout != F.pin || bits(p) != bits(vp[k])) F.pout[o] = p;
+            if (F.qout != F.qin || bits(q) != bits(vq[k])) F.qout[o] = q;
+            T dv = w - rest;  // blow-up deviation (stepper.py:295)
+            dv = dv < T(0) ? -dv : dv;
+            if (dv != dv) r.nan = 1;
+            else if (dv > r.dev) r.dev = dv;
+            if (!(isfinite(w) & isfinite(p) & isfinite(q))) {
+                const unsigned long long lin = (unsigned long long)(J - GL) * nx + (I - GL);
+                if (!isfinite(w)) atomicMin(&F.res->state_bad[0], lin);
+                if (!isfinite(p)) atomicMin(&F.res->state_bad[1], lin);
+                if (!isfinite(q)) atomicMin(&F.res->state_bad[2], lin);
+            }
+            extrema_cell(C, w, p, q, be, r);
+        }
     }
-#pragma unroll
-    for (int k = 0; k < FR; k++) {
-        const int J = GL + (blockIdx.y * FR + k) * FY + threadIdx.y;
-        if (I >= nx + GL || J >= ny + GL) continue;
-        const long o = L.at(J, I);
-        const T be = vbe[k];
-        T w = vw[k];
-        T p = vp[k], q = vq[k];
-        // clamp and volume tally (stepper.py:281-285); np.maximum keeps NaN
-        const T def = be - w;
-        if (def > T(0) || def != def) r.clamp = r.clamp + double(def);
-        w = (w >= be || w != w) ? w : be;
-        // film cutoff (stepper.py:288-292)
-        if (C.h_dry > T(0) && (w - be) < C.h_dry) {
-            p = T(0);
-            q = T(0);
-        }
-        const T rest = C.ws > be ? C.ws : be;  // np.maximum(ws, bed_eff)
-#pragma unroll
-        for (int side = 0; side < 4; side++) {  // sponge bands, order N, S, E, W
-            // band in local coordinates (a strip may hold part of a N/S band)
-            if (C.sponge_len[side] == 0) continue;
-            const int kk = (side == SIDE_E || side == SIDE_W) ? (I - GL) - C.sponge_lo[side]
-                                                              : (J - GL) - C.sponge_lo[side];
-            if (kk < 0 || kk >= C.sponge_len[side]) continue;
-            const T fac = F.fac[side][kk];
-            w = rest + (w - rest) * fac;
-            p = p * fac;
-            q = q * fac;
-        }
-        // the solves left P, Q in place and w* is already the pending w: store
-        // only what the clamp, film cutoff or sponge changed (bit patterns
-        // compared, so a zero's sign is kept exactly)
-        if (bits(w) != bits(vw[k])) F.w[o] = w;
-        if (F.pout != F.pin || bits(p) != bits(vp[k])) F.pout[o] = p;
-        if (F.qout != F.qin || bits(q) != bits(vq[k])) F.qout[o] = q;
-        T dv = w - rest;  // blow-up deviation (stepper.py:295)
-        dv = dv < T(0) ? -dv : dv;
-        if (dv != dv) r.nan = 1;
-        else if (double(dv) > r.dev) r.dev = double(dv);
-        const unsigned long long lin = (unsigned long long)(J - GL) * nx + (I - GL);
-        if (!(isfinite(w) & isfinite(p) & isfinite(q))) {
-            if (!isfinite(w)) atomicMin(&F.res->state_bad[0], lin);
-            if (!isfinite(p)) atomicMin(&F.res->state_bad[1], lin);
-            if (!isfinite(q)) atomicMin(&F.res->state_bad[2], lin);
-        }
-        extrema_cell(C, w, p, q, be, r);
-    }
-    r = red_block(r);
+    Red rr = red_block_warped(red_warp(r));
     const int tid = threadIdx.y * FX + threadIdx.x;
     const int nblk = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
     if (tid == 0) {
         Partial pt;
-        pt.max_rate = r.rate;
-        pt.max_speed = r.speed;
-        pt.max_depth = r.depth;
-        pt.max_dev = r.dev;
-        pt.clamped = r.clamp;
-        pt.dev_nan = r.nan;
+        pt.max_rate = rr.rate;
+        pt.max_speed = rr.speed;
+        pt.max_depth = rr.depth;
+        pt.max_dev = rr.dev;
+        pt.clamped = rr.clamp;
+        pt.dev_nan = rr.nan;
         pt.pad_ = 0;
         F.part[bid] = pt;
         __threadfence();
@@ -280,14 +347,14 @@ __global__ void __launch_bounds__(FT) k_extrema(Consts<T> C, const T *w, const T
                                                 const T *be, Partial *part) {
     const Layout L = C.L;
     const int I = GL + blockIdx.x * FX + threadIdx.x;
-    Red r{0, 0, 0, 0, 0, 0};
+    Acc<T> a{T(0), T(0), T(0), T(0), 0.0, 0};
     for (int k = 0; k < FR; k++) {
-        const int J = GL + (blockIdx.y * FR + k) * FY + threadIdx.y;
+        const int J = GL + blockIdx.y * FR * FY + k * FY + threadIdx.y;
         if (I >= L.nx + GL || J >= L.ny + GL) continue;
         const long o = L.at(J, I);
-        extrema_cell(C, w[o], p[o], q[o], be[o], r);
+        extrema_cell(C, w[o], p[o], q[o], be[o], a);
     }
-    r = red_block(r);
+    const Red r = red_block_warped(red_warp(a));
     if (threadIdx.x == 0 && threadIdx.y == 0) {
         Partial pt{};
         pt.max_rate = r.rate;
@@ -324,10 +391,12 @@ __global__ void k_fold_max(Consts<T> C, const T *w, T *maxw) {
 
 static dim3 final_grid(int nx, int ny) { return dim3((nx + FX - 1) / FX, (ny + FY * FR - 1) / (FY * FR)); }
 
+#if BSQ_INST_F64
 int final_blocks(int nx, int ny) {
     dim3 g = final_grid(nx, ny);
     return (int)(g.x * g.y);
 }
+#endif
 
 template <class T>
 void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st) {
@@ -351,19 +420,35 @@ void launch_fold_max(const Consts<T> &C, const T *w, T *maxw, cudaStream_t st) {
     k_fold_max<T><<<dim3((C.L.nx + 255) / 256, C.L.ny), 256, 0, st>>>(C, w, maxw);
 }
 
+#if BSQ_INST_F64
 template void launch_gather<double>(const double *, const double *, const double *,
                                     const long long *, int, double *, cudaStream_t);
+#endif
+#if BSQ_INST_F32
 template void launch_gather<float>(const float *, const float *, const float *,
                                    const long long *, int, float *, cudaStream_t);
+#endif
+#if BSQ_INST_F64
 template void launch_fold_max<double>(const Consts<double> &, const double *, double *,
                                       cudaStream_t);
+#endif
+#if BSQ_INST_F32
 template void launch_fold_max<float>(const Consts<float> &, const float *, float *, cudaStream_t);
+#endif
+#if BSQ_INST_F64
 template void launch_final<double>(const Consts<double> &, const FinalPtrs<double> &,
                                    cudaStream_t);
+#endif
+#if BSQ_INST_F64
 template void launch_extrema<double>(const Consts<double> &, const double *, const double *,
                                      const double *, const double *, Partial *, cudaStream_t);
+#endif
+#if BSQ_INST_F32
 template void launch_final<float>(const Consts<float> &, const FinalPtrs<float> &, cudaStream_t);
+#endif
+#if BSQ_INST_F32
 template void launch_extrema<float>(const Consts<float> &, const float *, const float *,
                                     const float *, const float *, Partial *, cudaStream_t);
+#endif
 
 }  // namespace bsq

@@ -124,12 +124,18 @@ void launch_frame(const Consts<T> &C, T *w, T *p, T *q, T *buf, int save, cudaSt
     k_frame<T><<<(n + 255) / 256, 256, 0, st>>>(C, w, p, q, buf, save);
 }
 
+#if BSQ_INST_F64
 size_t frame_elems(int nx, int ny) { return 3 * ((size_t)4 * (nx + 4) + (size_t)4 * ny); }
+#endif
 
+#if BSQ_INST_F64
 template void launch_frame<double>(const Consts<double> &, double *, double *, double *, double *,
                                    int, cudaStream_t);
+#endif
+#if BSQ_INST_F32
 template void launch_frame<float>(const Consts<float> &, float *, float *, float *, float *, int,
                                   cudaStream_t);
+#endif
 
 template <class T>
 void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
@@ -138,11 +144,15 @@ void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw
     k_ghost<T><<<(n + 127) / 128, 128, 0, st>>>(C, P, which, sw, sp, sq, dw, dp, dq);
 }
 
+#if BSQ_INST_F64
 template void launch_ghost<double>(const Consts<double> &, const DevParams *, int, const double *,
                                    const double *, const double *, double *, double *, double *,
                                    cudaStream_t);
+#endif
+#if BSQ_INST_F32
 template void launch_ghost<float>(const Consts<float> &, const DevParams *, int, const float *,
                                   const float *, const float *, float *, float *, float *,
                                   cudaStream_t);
+#endif
 
 }  // namespace bsq

@@ -329,11 +329,17 @@ void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
         k_solve_tma<T, false, false><<<g, b, smem, st>>>(C, M, S, bx, mode);
 }
 
+#if BSQ_INST_F64
 int solve_chunk_elems(int elem_bytes) { return 128 / elem_bytes; }
+#endif
 
+#if BSQ_INST_F64
 template void launch_solve<double>(const Consts<double> &, const SolveMaps &,
                                    const SolvePtrs<double> &, int, cudaStream_t, int);
+#endif
+#if BSQ_INST_F32
 template void launch_solve<float>(const Consts<float> &, const SolveMaps &,
                                   const SolvePtrs<float> &, int, cudaStream_t, int);
+#endif
 
 }  // namespace bsq

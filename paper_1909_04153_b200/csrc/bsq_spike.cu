@@ -98,11 +98,15 @@ void launch_spike(const Consts<T> &C, int G, int rank, const double *table, cons
     k_spike_fix<T><<<grd, blk, 0, st>>>(C, x, v, w, bt, south, north);
 }
 
+#if BSQ_INST_F64
 template void launch_spike<double>(const Consts<double> &, int, int, const double *,
                                    const double *, double *, double *, const double *,
                                    const double *, int, int, cudaStream_t);
+#endif
+#if BSQ_INST_F32
 template void launch_spike<float>(const Consts<float> &, int, int, const double *, const float *,
                                   float *, float *, const float *, const float *, int, int,
                                   cudaStream_t);
+#endif
 
 }  // namespace bsq

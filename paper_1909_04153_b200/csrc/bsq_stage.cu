@@ -365,9 +365,13 @@ void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A,
     }
 }
 
+#if BSQ_INST_F64
 template void launch_stage<double>(const Consts<double> &, const DevParams *,
                                    const StagePtrs<double> &, int, cudaStream_t, const StageMaps *);
+#endif
+#if BSQ_INST_F32
 template void launch_stage<float>(const Consts<float> &, const DevParams *,
                                   const StagePtrs<float> &, int, cudaStream_t, const StageMaps *);
+#endif
 
 }  // namespace bsq

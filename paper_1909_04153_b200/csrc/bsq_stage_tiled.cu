@@ -340,11 +340,15 @@ void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<
     tiled::k_stage<T><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, A, predict, *M);
 }
 
+#if BSQ_INST_F64
 template void launch_stage_tiled<double>(const Consts<double> &, const DevParams *,
                                          const StagePtrs<double> &, int, cudaStream_t,
                                          const StageMaps *);
+#endif
+#if BSQ_INST_F32
 template void launch_stage_tiled<float>(const Consts<float> &, const DevParams *,
                                         const StagePtrs<float> &, int, cudaStream_t,
                                         const StageMaps *);
+#endif
 
 }  // namespace bsq

@@ -28,12 +28,18 @@ def ncu_csv(args):
     return list(csv.reader(io.StringIO(out)))
 
 
+BYTE_UNITS = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0,
+              "GB": 1e9, "MB": 1e6, "KB": 1e3, "B": 1.0}
+TIME_MS = {"msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6, "second": 1e3,
+           "ms": 1.0, "us": 1e-3, "ns": 1e-6, "s": 1e3}
+
+
 def short(name: str) -> str:
     base = name.split("(")[0].replace("void ", "").replace("bsq::", "")
     return base
 
 
-def summary(rep: str, cells: int) -> str:
+def summary(rep: str, cells: int, mix: str = None) -> str:
     rows = ncu_csv(["-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)])
     hdr, units = rows[0], rows[1]
     lines = ["| kernel | ms | DRAM GB (r+w) | bytes/cell | DRAM % peak | fp64 pipe % | warps active % | regs | warp-inst/cell |",
@@ -41,11 +47,10 @@ def summary(rep: str, cells: int) -> str:
     heavy = None
     for r in rows[2:]:
         d = dict(zip(hdr, r))
-        ms = float(d["gpu__time_duration.sum"])
-        gb = float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])
-        u = dict(zip(hdr, units))["dram__bytes_read.sum"]
-        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(u, 1e9)
-        byts = gb * scale
+        un = dict(zip(hdr, units))
+        ms = float(d["gpu__time_duration.sum"]) * TIME_MS.get(un["gpu__time_duration.sum"], 1.0)
+        byts = (float(d["dram__bytes_read.sum"]) * BYTE_UNITS.get(un["dram__bytes_read.sum"], 1e9)
+                + float(d["dram__bytes_write.sum"]) * BYTE_UNITS.get(un["dram__bytes_write.sum"], 1e9))
         inst = float(d["smsp__inst_executed.sum"])
         lines.append(f"| {short(d['Kernel Name'])} | {ms:.3f} | {byts / 1e9:.3f} | {byts / cells:.1f} | "
                      f"{float(d['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']):.1f} | "
@@ -55,7 +60,7 @@ def summary(rep: str, cells: int) -> str:
         if heavy is None or ms > heavy[1]:
             heavy = (d["Kernel Name"], ms)
     if heavy:
-        k = short(heavy[0]).split("<")[0].split("::")[-1]
+        k = mix or short(heavy[0]).split("<")[0].split("::")[-1]
         sass = ncu_csv(["-i", rep, "--page", "source", "--csv", "-k", f"regex:{k}",
                         "--print-source", "sass"])
         h = sass[1]
@@ -109,8 +114,10 @@ def traffic_json(rep: str, cells: int, source: str) -> dict:
     fp64-pipe utilisation, for bench.py's roofline.traffic."""
     rows = ncu_csv(["-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)])
     hdr, units = rows[0], rows[1]
-    unit = dict(zip(hdr, units))["dram__bytes_read.sum"]
-    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(unit, 1e9)
+    un = dict(zip(hdr, units))
+    sr = BYTE_UNITS.get(un["dram__bytes_read.sum"], 1e9)
+    sw = BYTE_UNITS.get(un["dram__bytes_write.sum"], 1e9)
+    tms = TIME_MS.get(un["gpu__time_duration.sum"], 1.0)
     names = {"k_stage": "stage", "k_correct": "correct", "k_final": "final"}
     out, seen_solve = {}, 0
     for r in rows[2:]:
@@ -123,9 +130,9 @@ def traffic_json(rep: str, cells: int, source: str) -> dict:
             key = names.get(k)
         if not key or key in out:
             continue
-        b = (float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * scale
+        b = float(d["dram__bytes_read.sum"]) * sr + float(d["dram__bytes_write.sum"]) * sw
         out[key] = {"bytes_per_launch": b, "bytes_per_cell": b / cells,
-                    "ms": float(d["gpu__time_duration.sum"]),
+                    "ms": float(d["gpu__time_duration.sum"]) * tms,
                     "fp64_pipe_pct": float(d["sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"])}
     return {"source": source, "cells": cells, "kernels": out}
 
@@ -135,6 +142,7 @@ if __name__ == "__main__":
     ap.add_argument("rep", nargs="?")
     ap.add_argument("--cells", type=int, default=4096 * 4096)
     ap.add_argument("--launches")
+    ap.add_argument("--mix", help="kernel name (regex) for the opcode mix; default the heaviest")
     ap.add_argument("--traffic-json", help="write per-kernel DRAM bytes (for bench.py) here")
     a = ap.parse_args()
     if a.traffic_json:
@@ -144,4 +152,4 @@ if __name__ == "__main__":
     if a.launches:
         print(launches(a.launches))
     if a.rep:
-        print(summary(a.rep, a.cells))
+        print(summary(a.rep, a.cells, a.mix))
