@@ -32,15 +32,21 @@
 namespace bsq {
 
 constexpr int NLINE = 32;  // lines per CTA
-constexpr int NS = 6;      // forward ring depth (stages of 4 tiles)
-constexpr int NS2 = 12;    // backward ring depth (stages of 2 tiles), same bytes
+#ifndef BSQ_SOLVE_NS_ONCHIP
+#define BSQ_SOLVE_NS_ONCHIP 4
+#endif
 
-template <class T>
+// Ring geometry.  A forward stage holds FT tiles {r, a, den[, rden]}; the
+// backward pass reuses the same bytes as NS2 stages of 2 tiles {dw, cw}.
+template <class T, bool ONCHIP>
 struct TileGeom {
     static constexpr int EK = 128 / sizeof(T);              // elements per chunk (one 128-B row)
     static constexpr int TILE = NLINE * EK;                  // elements per tile
     static constexpr int TILE_B = TILE * sizeof(T);          // 4096 bytes
-    static constexpr int RING_B = NS * 4 * TILE_B;           // == NS2 * 2 * TILE_B
+    static constexpr int FT = ONCHIP ? 3 : 4;                // tiles per forward stage
+    static constexpr int NS = ONCHIP ? BSQ_SOLVE_NS_ONCHIP : 6;  // forward ring depth
+    static constexpr int NS2 = NS * FT / 2;                  // backward ring depth
+    static constexpr int RING_B = NS * FT * TILE_B;
     static constexpr int SMEM_B = 1024 + RING_B + 2 * TILE_B + 8 * (2 * NS + 2 * NS2);
 };
 
@@ -50,7 +56,7 @@ __device__ __forceinline__ int toff(int ln, int k) {
     if (XDIR) {  // box {EK, 32}: row = line, 128-B swizzle of 16-B units by (row & 7)
         constexpr int PER16 = 16 / sizeof(T);
         const int unit = (k / PER16) ^ (ln & 7);
-        return ln * TileGeom<T>::EK + unit * PER16 + (k % PER16);
+        return ln * (128 / (int)sizeof(T)) + unit * PER16 + (k % PER16);
     }
     return k * NLINE + ln;  // box {32, EK}: row = element
 }
@@ -67,8 +73,8 @@ __device__ __forceinline__ int toff(int ln, int k) {
 template <class T, bool XDIR, bool POS, bool RDEN_ONCHIP>
 __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
                                 int line0, unsigned char *smem, int mode) {
-    using G = TileGeom<T>;
-    constexpr int EK = G::EK, TILE = G::TILE;
+    using G = TileGeom<T, RDEN_ONCHIP>;
+    constexpr int EK = G::EK, TILE = G::TILE, NS = G::NS, NS2 = G::NS2, FT = G::FT;
     const Layout L = C.L;
     const int n = XDIR ? L.nx : L.ny;
     const int nlines = XDIR ? L.ny : L.nx;
@@ -77,7 +83,7 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
     const bool sint = !XDIR && S.south_int, nint = !XDIR && S.north_int;
     if (XDIR) mode = SOLVE_FULL;
 
-    T *ring = reinterpret_cast<T *>(smem);                    // NS x {r, a, den, rden}
+    T *ring = reinterpret_cast<T *>(smem);                    // NS x {r, a, den[, rden]}
     T *outb = reinterpret_cast<T *>(smem + G::RING_B);        // 2 out tiles
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + G::RING_B + 2 * G::TILE_B);
     uint64_t *empty = full + NS;
@@ -111,7 +117,7 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                 if (c >= NS) mbar_wait(&empty[s], ((c / NS) - 1) & 1);
                 int c0, c1;
                 coords(c, c0, c1);
-                T *st = ring + s * 4 * TILE;
+                T *st = ring + s * FT * TILE;
                 if (RDEN_ONCHIP) {
                     mbar_expect_tx(&full[s], 3 * G::TILE_B);
                 } else {
@@ -149,7 +155,7 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
         T dw = T(0);
         for (int c = 0; c < nc; c++) {
             const int s = c % NS;
-            T *st = ring + s * 4 * TILE;
+            T *st = ring + s * FT * TILE;
             T *ob = outb + (c & 1) * TILE;
             if (lane == 0) bulk_wait_read<1>();  // the store from this out tile (c-2) has read it
             __syncwarp();
@@ -302,13 +308,13 @@ template <class T>
 void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, int pivots,
                   cudaStream_t st, int mode) {
     const int nbx = (C.L.ny + NLINE - 1) / NLINE, nby = (C.L.nx + NLINE - 1) / NLINE;
-    const int smem = TileGeom<T>::SMEM_B;
+    const int smem_on = TileGeom<T, true>::SMEM_B, smem_off = TileGeom<T, false>::SMEM_B;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_solve_tma<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_solve_tma<T, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_solve_tma<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_solve_tma<T, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_solve_tma<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_on);
+        cudaFuncSetAttribute(k_solve_tma<T, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_on);
+        cudaFuncSetAttribute(k_solve_tma<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_off);
+        cudaFuncSetAttribute(k_solve_tma<T, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_off);
         attr_set = true;
     }
     const int bx = mode == SOLVE_YBWD ? 0 : nbx;  // x-line CTAs in this launch
@@ -320,13 +326,13 @@ void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
 #endif
     dim3 g(bx + nby), b(64);
     if (pos && onchip)
-        k_solve_tma<T, true, true><<<g, b, smem, st>>>(C, M, S, bx, mode);
+        k_solve_tma<T, true, true><<<g, b, smem_on, st>>>(C, M, S, bx, mode);
     else if (pos)
-        k_solve_tma<T, true, false><<<g, b, smem, st>>>(C, M, S, bx, mode);
+        k_solve_tma<T, true, false><<<g, b, smem_off, st>>>(C, M, S, bx, mode);
     else if (onchip)
-        k_solve_tma<T, false, true><<<g, b, smem, st>>>(C, M, S, bx, mode);
+        k_solve_tma<T, false, true><<<g, b, smem_on, st>>>(C, M, S, bx, mode);
     else
-        k_solve_tma<T, false, false><<<g, b, smem, st>>>(C, M, S, bx, mode);
+        k_solve_tma<T, false, false><<<g, b, smem_off, st>>>(C, M, S, bx, mode);
 }
 
 #if BSQ_INST_F64
