@@ -287,6 +287,9 @@ def main():
     ms_step = ms_total / args.steps
     value = cells_total * args.steps / (ms_total * 1e-3) / 1e9
     kps = sim._dev.kernels_per_step()
+    # the clock samples of the timed region are all we need: stop nvidia-smi
+    # before the per-kernel, fp32 and e2e passes so it cannot perturb them
+    clock_info = clocks.stop(t_c0, t_c1)
     # per-kernel device times: the same steps again with CUDA events around
     # every kernel (kept out of the timed region above)
     sim._dev.set_timing(True)
@@ -363,7 +366,6 @@ def main():
                        "reductions) + final state download; excludes one-time setup "
                        "(static upload + LU factorization)"}
     sim.close()
-    clock_info = clocks.stop(t_c0, t_c1)
 
     # ---- CPU baseline (rank 0, N = 1 only) ------------------------------------------
     cpu = None

@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, Final
     const long rstep = (long)FY * L.pitch;
     const long o0 = L.at(J0, I);
     const bool iin = I < nx + GL;
+    const bool sponges = (C.sponge_len[0] | C.sponge_len[1] | C.sponge_len[2] | C.sponge_len[3]) != 0;
     Acc<T> r{T(0), T(0), T(0), T(0), 0.0, 0};
 #pragma unroll
     for (int k0 = 0; k0 < FR; k0 += FG) {
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, Final
             }
             const T rest = C.ws > be ? C.ws : be;  // np.maximum(ws, bed_eff)
 #pragma unroll
-            for (int side = 0; side < 4; side++) {  // sponge bands, order N, S, E, W
+            for (int side = 0; side < 4 && sponges; side++) {  // sponge bands, order N, S, E, W
                 // band in local coordinates (a strip may hold part of a N/S band)
                 if (C.sponge_len[side] == 0) continue;
                 const int kk = (side == SIDE_E || side == SIDE_W) ? (I - GL) - C.sponge_lo[side]

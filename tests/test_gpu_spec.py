@@ -124,3 +124,24 @@ def test_blowup_after_speculation_same_error_state():
         for f in ("w", "p", "q"):
             x, y = getattr(errs[0][k], f), getattr(errs[1][k], f)
             assert np.array_equal(x.view(np.uint64), y.view(np.uint64)), (k, f)
+
+
+def test_rejected_speculation_then_plain_steps_keep_ghosts():
+    """A speculation rejected by a caller-given dt, followed by steps that
+    queue none: every later state read (its ghost frame included) is the
+    non-speculative one -- the frame saved for the rejected speculation
+    must not come back when the buffers cycle round to the same slots."""
+    for read_each in (False, True):
+        a, b = _pair(make_case("C3", scale=8))
+        for _ in range(6):
+            assert a.advance() == b.advance()
+        assert a.advance(0.9 * a.controller.dt) == b.advance(0.9 * b.controller.dt)
+        a.speculate = False
+        for k in range(1, 10):
+            assert a.advance() == b.advance()
+            if read_each or k % 6 == 0 or k == 9:
+                _same_full_state(a, b)
+        a.speculate = True
+        for _ in range(4):
+            assert a.advance() == b.advance()
+            _same_full_state(a, b)
