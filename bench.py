@@ -350,18 +350,23 @@ def main():
     barrier()
     t0 = time.perf_counter()
     sim.state = FieldState(*pin)  # upload (a rank uploads its strip)
+    t_up = time.perf_counter()
     for _ in range(args.steps):
         sim.advance()
+    t_st = time.perf_counter()
     if world > 1:
         sim._dev.download_local(out=pin_out)  # each rank brings back its own strip
     else:
         sim.download_state(out=pin_out)
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    t_dn = time.perf_counter()
+    e2e_s = max_over_ranks(t_dn - t0)
     state_bytes = 3 * 8 * (cells_gpu + 4 * case.bathy.grid.nx)
     h2d = state_bytes / args.steps + ctypes.sizeof(nat.StepParams)
     d2h = state_bytes / args.steps + ctypes.sizeof(nat.StepResult)
     e2e = {"value": cells_total * args.steps / e2e_s / 1e9, "unit": "Gcell-updates/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+           "upload_ms": 1e3 * (t_up - t0), "steps_ms": 1e3 * (t_st - t_up),
+           "download_ms": 1e3 * (t_dn - t_st),
            "includes": "state upload from pinned host + K advance() (H2D scalars, D2H "
                        "reductions) + final state download; excludes one-time setup "
                        "(static upload + LU factorization)"}

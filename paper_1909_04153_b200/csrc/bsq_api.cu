@@ -635,6 +635,10 @@ struct Engine : EngineBase {
         }
         CU(cudaEventCreateWithFlags(&ev_res, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&ev_frame, cudaEventDisableTiming));
+        if (F64) {  // the overlapped state download (download_beside_spec)
+            CU(cudaStreamCreateWithFlags(&st_io, cudaStreamNonBlocking));
+            CU(cudaMallocHost(&hframe, sizeof(T) * frame_elems(d.nx, d.ny)));
+        }
         set_consts();
         const int nx = d.nx, ny = d.ny;
         CU(cudaMemsetAsync(workspace, 0, need, st));  // ghost cells of scratch arrays stay defined
@@ -698,8 +702,6 @@ struct Engine : EngineBase {
     // host arrays.  The device keeps the frame the queued stage needs.
     int download_beside_spec(int s, double *w, double *p, double *q) {
         const int ny = d.ny, nx = d.nx, W_ = nx + 4, nrow = 4 * W_, n = nrow + 4 * ny;
-        if (!st_io) CU(cudaStreamCreateWithFlags(&st_io, cudaStreamNonBlocking));
-        if (!hframe) CU(cudaMallocHost(&hframe, sizeof(T) * 3 * (size_t)n));
         CU(cudaStreamWaitEvent(st_io, ev_res, 0));
         double *dst[3] = {w, p, q};
         const T *src[3] = {W(s), Pp(s), Qq(s)};
