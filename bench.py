@@ -347,6 +347,12 @@ def main():
            for a in (case.state.w, case.state.p, case.state.q)]
     sim = make_sim(state=FieldState(*pin))
     pin_out = [torch.empty(a.shape, dtype=torch.float64).pin_memory().numpy() for a in pin]
+    # both pinned buffers have been used once before the timed region (the
+    # constructor uploaded from pin): bring the state back into pin_out once
+    if world > 1:
+        sim._dev.download_local(out=pin_out)
+    else:
+        sim.download_state(out=pin_out)
     barrier()
     t0 = time.perf_counter()
     sim.state = FieldState(*pin)  # upload (a rank uploads its strip)
