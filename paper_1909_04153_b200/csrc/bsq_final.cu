@@ -129,8 +129,8 @@ __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, 
     // which never raises a maximum: skip it (whole dry warps branch over)
     if (!(w - be > T(0)) && p == T(0) && q == T(0)) return;
     T h = w - be;
-    if (h < T(0)) h = T(0);
-    const T hstar = h > C.h_eps ? h : C.h_eps;
+    h = floor0(h);
+    const T hstar = floor_eps(h, C.h_eps);
     const T c = sqrt(C.g * h);
     const T nrh = -rcp_rn(hstar);  // both quotients correctly rounded via one reciprocal
     const T su = div_nonneg(fabs(p), hstar, nrh) + c;

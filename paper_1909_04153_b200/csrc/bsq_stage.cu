@@ -227,8 +227,8 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
             const T src_x = -g * (wc - T(0.5) * (bx_e + bx_w)) * (bx_e - bx_w) * C.inv_dx;
             const T src_y = -g * (wc - T(0.5) * (bfy_n + bfy_s)) * (bfy_n - bfy_s) * C.inv_dy;
             T h = wc - c_be;
-            if (h < T(0)) h = T(0);
-            const T hstar = h > h_eps ? h : h_eps;
+            h = floor0(h);
+            const T hstar = floor_eps(h, h_eps);
             T fric = T(0);
             if (C.c_f > T(0)) fric = C.c_f * sqrt(pc * pc + qc * qc) / (hstar * hstar);
             T rp = -(fe_2 - fw2) * C.inv_dx - (fn2 - fs2) * C.inv_dy + src_x - fric * pc;

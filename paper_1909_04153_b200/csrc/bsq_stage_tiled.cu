@@ -223,8 +223,8 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     const T src_x = -C.g * (wc - T(0.5) * (be_ + bw_)) * (be_ - bw_) * C.inv_dx;
     const T src_y = -C.g * (wc - T(0.5) * (bn_ + bs_)) * (bn_ - bs_) * C.inv_dy;
     T h = wc - S.be[y][x];
-    if (h < T(0)) h = T(0);
-    const T hstar = h > C.h_eps ? h : C.h_eps;
+    h = floor0(h);
+    const T hstar = floor_eps(h, C.h_eps);
     T fric = T(0);
     if (C.c_f > T(0)) fric = C.c_f * sqrt(pc * pc + qc * qc) / (hstar * hstar);
     T rp = -(S.u.x.fx[1][ty][tx + 1] - S.u.x.fx[1][ty][tx]) * C.inv_dx -
