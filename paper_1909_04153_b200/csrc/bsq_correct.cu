@@ -10,13 +10,19 @@ namespace bsq {
 // Cross-correction right-hand sides (stepper.py:268-273):
 //   us_corr = base_u + (F*(P1, Q1) - F*_n),  vs_corr = base_v + (G*(P1, Q1) - G*_n)
 // written over us / vs.
-// Each thread owns CR consecutive cells of one column; the 3-column window
+// Each thread owns CR consecutive cells of one column (2 in fp64, 4 in fp32:
+// 0.140 -> 0.135 ms; 8 rows 0.203 ms); the 3-column window
 // of P1 and Q1 over rows J-1 .. J+CR is loaded once and shared, and every
 // load is issued before any arithmetic: the kernel is a pure stream.
-constexpr int CR = 2;
+#ifndef BSQ_CORRECT_CR32
+#define BSQ_CORRECT_CR32 4
+#endif
+template <class T>
+__host__ __device__ constexpr int cr_rows() { return sizeof(T) == 8 ? 2 : BSQ_CORRECT_CR32; }
 
 template <class T>
 __global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) {
+    constexpr int CR = cr_rows<T>();
     const Layout L = C.L;
     const int I = GL + blockIdx.x * 32 + threadIdx.x;
     const int J0 = GL + (blockIdx.y * 8 + threadIdx.y) * CR;
@@ -74,6 +80,7 @@ __global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) 
 
 template <class T>
 void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st) {
+    constexpr int CR = cr_rows<T>();
     dim3 grid((C.L.nx + 31) / 32, (C.L.ny + 8 * CR - 1) / (8 * CR));  // 32 x (8*CR) cells
     k_correct<T><<<grid, dim3(32, 8), 0, st>>>(C, K);
 }
