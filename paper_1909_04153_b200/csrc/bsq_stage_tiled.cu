@@ -226,7 +226,10 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     h = floor0(h);
     const T hstar = floor_eps(h, C.h_eps);
     T fric = T(0);
-    if (C.c_f > T(0)) fric = C.c_f * sqrt(pc * pc + qc * qc) / (hstar * hstar);
+    if (C.c_f > T(0)) {  // c_f sqrt(P^2 + Q^2) / h*^2, the quotient via RN(1/h*^2) (div_rcp)
+        const T h2 = hstar * hstar;
+        fric = div_rcp(C.c_f * sqrt(pc * pc + qc * qc), h2, rcp_rn(h2));
+    }
     T rp = -(S.u.x.fx[1][ty][tx + 1] - S.u.x.fx[1][ty][tx]) * C.inv_dx -
            (S.u.x.fy[1][ty + 1][tx] - S.u.x.fy[1][ty][tx]) * C.inv_dy + src_x - fric * pc;
     T rq = -(S.u.x.fx[2][ty][tx + 1] - S.u.x.fx[2][ty][tx]) * C.inv_dx -
