@@ -236,6 +236,7 @@ def main():
         dist = dist_mod
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()  # communicator up on every rank before the first P2P exchange
         comm = DistComm()
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
