@@ -10,9 +10,10 @@ kernels emit none) and the default IEEE division / square root
 
 Every kernel source is compiled twice: once for the fp64 kernels with the
 flags above (-DBSQ_TU_F64), once for the fp32 kernels (-DBSQ_TU_F32
--DBSQ_FAST_F32) with approximate single-precision division and square root,
-flush-to-zero and (except where fp64 controller arithmetic shares the file)
-contracted multiply-adds: the fp32 mode's contract is a tolerance, not bits.
+-DBSQ_FAST_F32) with approximate single-precision square root and plain
+division, flush-to-zero and (except where fp64 controller arithmetic shares
+the file) contracted multiply-adds: the fp32 mode's contract is a tolerance,
+not bits.  Its Markstein quotients stay correctly rounded (accuracy).
 """
 
 from __future__ import annotations
@@ -62,7 +63,7 @@ def flags_for(src: str, prec: str) -> list:
         fl += ["-prec-div=false", "-prec-sqrt=false", "-ftz=true",
                "--fmad=false" if src in F32_NO_CONTRACT else "--fmad=true",
                "-DBSQ_TU_F32", "-DBSQ_FAST_F32"]
-        return fl
+        return fl + os.environ.get("BSQ_F32_EXTRA", "").split()  # A/B builds only
     return list(FLAGS)
 
 
