@@ -36,8 +36,14 @@
 namespace bsq {
 
 constexpr int SW_ = 32;          // columns per CTA (one per lane)
-constexpr int SNW = 4;           // warps per CTA
-constexpr int SR = 8;            // rows per warp
+#ifndef BSQ_CW_WARPS
+#define BSQ_CW_WARPS 4
+#endif
+#ifndef BSQ_CW_ROWS
+#define BSQ_CW_ROWS 4
+#endif
+constexpr int SNW = BSQ_CW_WARPS;  // warps per CTA
+constexpr int SR = BSQ_CW_ROWS;    // rows per warp
 constexpr int STY = SNW * SR;    // rows per CTA
 constexpr int SHX = SW_ + 4, SHY = STY + 4;
 constexpr unsigned FULL = 0xffffffffu;
