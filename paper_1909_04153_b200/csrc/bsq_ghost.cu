@@ -2,12 +2,14 @@
 //
 // A step launches, in order (see DESIGN.md for the HBM budget of each):
 //   k_ghost      ghost strips at t                       (boundary.py:316-323)
-//   k_stage      fused stage set + predictor             (bsq_stage.cu)
+//   k_stage      fused stage set + predictor             (bsq_stage_tiled.cu / bsq_stage.cu)
 //   k_ghost      strips of the predicted state at t+dt   (stepper.py:252-254)
-//   k_solve_pipe first x/y line solves                   (bsq_solve.cu)
-//   k_correct    cross-correction right-hand sides       (bsq_solve.cu)
-//   k_solve_pipe second x/y line solves
+//   k_solve_tma  first x/y line solves                   (bsq_solve.cu)
+//   k_correct    cross-correction right-hand sides       (bsq_correct.cu)
+//   k_solve_tma  second x/y line solves
 //   k_final      clamp, film, sponge, checks, extrema    (bsq_final.cu)
+// and, when the next stage is queued early, k_frame (save of this state's
+// ghost frame) + the next step's k_ghost and k_stage.
 #include <cfloat>
 #include <cmath>
 #include <cstdint>

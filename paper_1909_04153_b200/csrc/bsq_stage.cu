@@ -350,9 +350,9 @@ void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<
                         cudaStream_t st, const StageMaps *M);
 
 // fp64 runs the tiled variant (bsq_stage_tiled.cu: 64 registers, 32 warps per
-// SM, 1.31 ms at 4096^2) -- the column walk needs 128 fp64 registers and
-// loses on latency hiding (1.35 ms); fp32 runs the column walk (71
-// registers; 1.50 vs 1.66 ms per step).  Measured A/B on B200, round 1.
+// SM) -- the column walk needs 128 fp64 registers and loses on latency hiding
+// (1.317 vs 1.114 ms at 4096^2); fp32 runs the column walk (72 registers;
+// tiled 0.821 vs 0.722 ms).  Measured A/B on B200, round 1.
 template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
                   cudaStream_t st, const StageMaps *M) {
