@@ -25,11 +25,12 @@ ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--precision", default="fp64")
 ap.add_argument("--case", default="C4")
 ap.add_argument("--no-spec", action="store_true", help="do not queue the next stage early")
+ap.add_argument("--solver", default="thomas")
 a = ap.parse_args()
 case = make_case(a.case)
 sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
                         stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
-                        precision=a.precision)
+                        precision=a.precision, solver=a.solver)
 sim.speculate = not a.no_spec
 for _ in range(4):
     sim.advance()
