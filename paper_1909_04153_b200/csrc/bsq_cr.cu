@@ -19,7 +19,18 @@
 
 namespace bsq {
 
-constexpr int CR_THREADS = 512;
+#ifndef BSQ_CR_THREADS
+#define BSQ_CR_THREADS 512
+#endif
+constexpr int CR_THREADS = BSQ_CR_THREADS;
+
+// Shared-memory slot of row i: the low 4 bits XOR-ed with bits 4-7 and 8-11.
+// A level touches rows s-1, 3s-1, ... (stride 2s); plain indexing puts 16
+// threads of a warp on one bank pair once 2s >= 16, this permutation keeps a
+// half-warp's 8-byte accesses on distinct bank pairs for every stride up to
+// 512 (a bijection within each block of 16 rows; placement only, so the
+// arithmetic and its results are unchanged).
+__device__ __forceinline__ int crs(int i) { return i ^ ((i >> 4) & 15) ^ ((i >> 8) & 15); }
 
 // line l of direction xdir: element e at padded (GL+l, GL+e) (x) or
 // (GL+e, GL+l) (y)
@@ -34,6 +45,7 @@ __device__ void cr_line(const Consts<T> &C, const CrPtrs<T> &K, int line, T *sm,
     const T *R = XDIR ? K.rx : K.ry;
     auto off = [&](int e) -> long { return XDIR ? L.at(GL + line, GL + e) : L.at(GL + e, GL + line); };
     // load + ghost folding (implicit.py:178-179 / :190-191), identity padding
+#pragma unroll 4
     for (int i = threadIdx.x; i < n2; i += blockDim.x) {
         if (i < n) {
             const long o = off(i);
@@ -46,15 +58,17 @@ __device__ void cr_line(const Consts<T> &C, const CrPtrs<T> &K, int line, T *sm,
                 const T g1 = XDIR ? K.gp[L.at(GL + line, n + GL)] : K.gq[L.at(n + GL, GL + line)];
                 rv = rv - Cc[o] * g1;
             }
-            a[i] = A[o];
-            b[i] = B[o];
-            c[i] = Cc[o];
-            r[i] = rv;
+            const int j = crs(i);
+            a[j] = A[o];
+            b[j] = B[o];
+            c[j] = Cc[o];
+            r[j] = rv;
         } else {
-            a[i] = T(0);
-            b[i] = T(1);
-            c[i] = T(0);
-            r[i] = T(0);
+            const int j = crs(i);
+            a[j] = T(0);
+            b[j] = T(1);
+            c[j] = T(0);
+            r[j] = T(0);
         }
     }
     __syncthreads();
@@ -63,16 +77,16 @@ __device__ void cr_line(const Consts<T> &C, const CrPtrs<T> &K, int line, T *sm,
     for (int stride = 1; stride < n2 / 2; stride *= 2) {
         const int step = 2 * stride;
         for (int k = threadIdx.x; k < n2 / step; k += blockDim.x) {
-            const int idx = step * k + step - 1;
-            const int il = idx - stride;
+            const int i0 = step * k + step - 1, ir0 = i0 + stride;
+            const int idx = crs(i0), il = crs(i0 - stride);
             if (b[il] == T(0)) kind = 0;
             const T alpha = -a[idx] / b[il];
             T aa = alpha * a[il];
             T bb = b[idx] + alpha * c[il];
             T rr = r[idx] + alpha * r[il];
             T cc;
-            const int ir = idx + stride;
-            if (ir < n2) {
+            if (ir0 < n2) {
+                const int ir = crs(ir0);
                 if (b[ir] == T(0)) kind = 0;
                 const T beta = -c[idx] / b[ir];
                 cc = beta * c[ir];
@@ -90,7 +104,7 @@ __device__ void cr_line(const Consts<T> &C, const CrPtrs<T> &K, int line, T *sm,
     }
     // 2x2 core (_kernels.py:435-441)
     if (threadIdx.x == 0) {
-        const int i1 = n2 / 2 - 1, i2 = n2 - 1;
+        const int i1 = crs(n2 / 2 - 1), i2 = crs(n2 - 1);
         const T det = b[i1] * b[i2] - c[i1] * a[i2];
         if (det == T(0) && kind > 1) kind = 1;
         x[i1] = (r[i1] * b[i2] - c[i1] * r[i2]) / det;
@@ -101,17 +115,17 @@ __device__ void cr_line(const Consts<T> &C, const CrPtrs<T> &K, int line, T *sm,
     for (int stride = n2 / 4; stride >= 1; stride /= 2) {
         const int step = 2 * stride;
         for (int k = threadIdx.x; k * step + stride - 1 < n2; k += blockDim.x) {
-            const int idx = step * k + stride - 1;
+            const int i0 = step * k + stride - 1, idx = crs(i0);
             if (b[idx] == T(0) && kind > 2) kind = 2;
-            const T lower = idx - stride >= 0 ? x[idx - stride] : T(0);
-            x[idx] = (r[idx] - a[idx] * lower - c[idx] * x[idx + stride]) / b[idx];
+            const T lower = i0 - stride >= 0 ? x[crs(i0 - stride)] : T(0);
+            x[idx] = (r[idx] - a[idx] * lower - c[idx] * x[crs(i0 + stride)]) / b[idx];
         }
         __syncthreads();
     }
     if (kind < 3)
         atomicMin(K.bad, K.key_base | (XDIR ? 0u : 1u << 30) | ((unsigned)line << 2) | kind);
     T *out = XDIR ? K.outx : K.outy;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) out[off(i)] = x[i];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[off(i)] = x[crs(i)];
 }
 
 template <class T>

@@ -22,11 +22,12 @@ ap.add_argument("--scale", type=int, default=1)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--case", default="C4")
 ap.add_argument("--precision", default="fp64")
+ap.add_argument("--solver", default="thomas")
 args = ap.parse_args()
 case = make_case(args.case, scale=args.scale)
 sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
                         stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
-                        precision=args.precision)
+                        precision=args.precision, solver=args.solver)
 for _ in range(3 + args.steps):
     rec = sim.advance()
 torch.cuda.synchronize()
