@@ -184,7 +184,13 @@ int bsq_fill_ghosts(bsq_ctx *ctx, const double *maker_eta, const double *maker_f
  *                  across ranks), synchronizes the stream */
 enum {
     BSQ_PH_GHOST = 0, BSQ_PH_STAGE = 1, BSQ_PH_SOLVE1F = 2, BSQ_PH_SOLVE1B = 3,
-    BSQ_PH_CORRECT = 4, BSQ_PH_SOLVE2F = 5, BSQ_PH_SOLVE2B = 6, BSQ_PH_FINAL = 7
+    BSQ_PH_CORRECT = 4, BSQ_PH_SOLVE2F = 5, BSQ_PH_SOLVE2B = 6, BSQ_PH_FINAL = 7,
+    /* BSQ_PH_STAGE / BSQ_PH_CORRECT split around their halo exchange: the
+     * INNER phase runs the rows that read no halo row (queue it while the
+     * halo is in flight), the EDGE phase the rest once the halo is in place
+     * (and, for the stage, the predicted-state ghosts) */
+    BSQ_PH_STAGE_INNER = 8, BSQ_PH_STAGE_EDGE = 9, BSQ_PH_CORRECT_INNER = 10,
+    BSQ_PH_CORRECT_EDGE = 11
 };
 int bsq_phase(bsq_ctx *ctx, int phase, const bsq_step_params *params, bsq_step_result *result);
 /* cw of this strip's last row, per column (nx): the next strip's cw_south */

@@ -244,6 +244,13 @@ struct Engine : EngineBase {
     bool g_fresh = false;   // g_com holds the committed state's values
     T *maxw = nullptr;      // padded layout, interior used
     bool fold_req = false;  // fold the committed state into maxw at the next stage
+    // strips: rows [lo, hi) of the stage / the correction read no halo row, so
+    // they run while the halo is in flight (BSQ_PH_*_INNER), the rest after
+    bool stage_inner = false, correct_inner = false;
+    void inner_rows(int reach, int &lo, int &hi) const {
+        lo = d.south_internal ? STAGE_BAND : 0;
+        hi = d.north_internal ? (d.ny - reach) / STAGE_BAND * STAGE_BAND : d.ny;
+    }
     SolveMaps maps;                  // TMA descriptors (out slots patched per launch)
     CUtensorMap map_xout[3], map_yout[3];  // pending P/Q of state 0, state 1; P2/Q2
 
@@ -994,6 +1001,68 @@ struct Engine : EngineBase {
                 launch_correct(C, correct_ptrs(slot, nxt), st);
                 ev_mark("correct");
             }
+            break;
+        case BSQ_PH_STAGE_INNER: {
+            // the stage reads rows J-2 .. J+2: rows >= 2 away from an internal
+            // side need none of the halo rows being exchanged
+            int lo, hi;
+            inner_rows(2, lo, hi);
+            stage_inner = !spec_used && hi > lo;
+            if (stage_inner) {
+                ++step_launches;
+                const StageMaps sm = stage_maps_for(W(cur), Pp(cur), Qq(cur));
+                launch_stage(C, dparams, stage_ptrs(slot), 1, st, &sm, lo, hi - lo);
+            }
+            break;
+        }
+        case BSQ_PH_STAGE_EDGE: {
+            if (!spec_used) {
+                const StageMaps sm = stage_maps_for(W(cur), Pp(cur), Qq(cur));
+                if (stage_inner) {
+                    int lo, hi;
+                    inner_rows(2, lo, hi);
+                    step_launches += (lo > 0) + (hi < d.ny);
+                    launch_stage(C, dparams, stage_ptrs(slot), 1, st, &sm, 0, lo);
+                    launch_stage(C, dparams, stage_ptrs(slot), 1, st, &sm, hi, d.ny - hi);
+                } else {
+                    ++step_launches;
+                    launch_stage(C, dparams, stage_ptrs(slot), 1, st, &sm);
+                }
+                fold_req = false;
+                ev_mark("stage");
+            }
+            stage_inner = false;
+            ++step_launches;
+            launch_ghost(C, dparams, 1, W(nxt), Pp(cur), Qq(cur), W(nxt), Pp(nxt), Qq(nxt), st);
+            ev_mark("ghost_n");
+            break;
+        }
+        case BSQ_PH_CORRECT_INNER: {
+            // the correction reads rows J-1 .. J+1 of the first-solve momenta
+            int lo, hi;
+            inner_rows(1, lo, hi);
+            correct_inner = d.cross_correction && hi > lo;
+            if (correct_inner) {
+                ++step_launches;
+                launch_correct(C, correct_ptrs(slot, nxt), st, lo, hi - lo);
+            }
+            break;
+        }
+        case BSQ_PH_CORRECT_EDGE:
+            if (d.cross_correction) {
+                if (correct_inner) {
+                    int lo, hi;
+                    inner_rows(1, lo, hi);
+                    step_launches += (lo > 0) + (hi < d.ny);
+                    launch_correct(C, correct_ptrs(slot, nxt), st, 0, lo);
+                    launch_correct(C, correct_ptrs(slot, nxt), st, hi, d.ny - hi);
+                } else {
+                    ++step_launches;
+                    launch_correct(C, correct_ptrs(slot, nxt), st);
+                }
+                ev_mark("correct");
+            }
+            correct_inner = false;
             break;
         case BSQ_PH_SOLVE2F:
             if (d.cross_correction) {

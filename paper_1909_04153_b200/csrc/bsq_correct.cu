@@ -21,11 +21,11 @@ template <class T>
 __host__ __device__ constexpr int cr_rows() { return sizeof(T) == 8 ? 2 : BSQ_CORRECT_CR32; }
 
 template <class T>
-__global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) {
+__global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K, int row0) {
     constexpr int CR = cr_rows<T>();
     const Layout L = C.L;
     const int I = GL + blockIdx.x * 32 + threadIdx.x;
-    const int J0 = GL + (blockIdx.y * 8 + threadIdx.y) * CR;
+    const int J0 = GL + row0 + (blockIdx.y * 8 + threadIdx.y) * CR;
     const long pitch = L.pitch;
     if (I >= L.nx + GL || J0 >= L.ny + GL) return;
     T d[CR], dx_[CR], dy_[CR], bu[CR], bv[CR], fs[CR], gs[CR], qw[CR + 2][3], pw[CR + 2][3];
@@ -79,19 +79,23 @@ __global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) 
 // launchers
 
 template <class T>
-void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st) {
+void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st, int row0,
+                    int nrows) {
     constexpr int CR = cr_rows<T>();
-    dim3 grid((C.L.nx + 31) / 32, (C.L.ny + 8 * CR - 1) / (8 * CR));  // 32 x (8*CR) cells
-    k_correct<T><<<grid, dim3(32, 8), 0, st>>>(C, K);
+    static_assert(STAGE_BAND % (8 * CR) == 0, "band of whole blocks");
+    if (nrows < 0) nrows = C.L.ny - row0;
+    if (nrows <= 0) return;
+    dim3 grid((C.L.nx + 31) / 32, (nrows + 8 * CR - 1) / (8 * CR));  // 32 x (8*CR) cells
+    k_correct<T><<<grid, dim3(32, 8), 0, st>>>(C, K, row0);
 }
 
 #if BSQ_INST_F64
 template void launch_correct<double>(const Consts<double> &, const CorrectPtrs<double> &,
-                                     cudaStream_t);
+                                     cudaStream_t, int, int);
 #endif
 #if BSQ_INST_F32
 template void launch_correct<float>(const Consts<float> &, const CorrectPtrs<float> &,
-                                    cudaStream_t);
+                                    cudaStream_t, int, int);
 #endif
 
 }  // namespace bsq

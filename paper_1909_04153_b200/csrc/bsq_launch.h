@@ -98,9 +98,12 @@ struct StageMaps {
 template <class T>
 void launch_frame(const Consts<T> &C, T *w, T *p, T *q, T *buf, int save, cudaStream_t st);
 size_t frame_elems(int nx, int ny);
+// rows [row0, row0 + nrows) of the interior (nrows < 0: to the last row);
+// row0 a multiple of STAGE_BAND
+constexpr int STAGE_BAND = 32;
 template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
-                  cudaStream_t st, const StageMaps *M = nullptr);
+                  cudaStream_t st, const StageMaps *M = nullptr, int row0 = 0, int nrows = -1);
 // pivot properties of a factored operator (launch_solve's `pivots`)
 enum { PIV_POSITIVE = 1, PIV_RDEN_INRANGE = 2 };
 template <class T>
@@ -110,8 +113,10 @@ int solve_chunk_elems(int elem_bytes);
 template <class T>
 void launch_cr(const Consts<T> &C, const CrPtrs<T> &K, cudaStream_t st);
 size_t cr_smem_bytes(int nx, int ny, int elem);
+// rows [row0, row0 + nrows) (nrows < 0: to the last row); row0 a multiple of STAGE_BAND
 template <class T>
-void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st);
+void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st, int row0 = 0,
+                    int nrows = -1);
 template <class T>
 void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st);
 template <class T>

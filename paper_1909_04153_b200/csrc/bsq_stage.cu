@@ -77,13 +77,13 @@ __device__ __forceinline__ T shfl_dn1(T v) { return __shfl_down_sync(FULL, v, 1)
 
 template <class T>
 __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevParams *__restrict__ P,
-                                                   StagePtrs<T> A, int predict) {
+                                                   StagePtrs<T> A, int predict, int row0) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StageSmem<T> &S = *reinterpret_cast<StageSmem<T> *>(smem_raw);
     const Layout L = C.L;
     const int nx = L.nx, ny = L.ny, nxt = nx + 4, nyt = ny + 4;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int I0 = GL + blockIdx.x * SW_, J0 = GL + blockIdx.y * STY;
+    const int I0 = GL + blockIdx.x * SW_, J0 = GL + row0 + blockIdx.y * STY;
 
     // ---- tile + 2-cell halo; eta = (w - bed_eff) - depth (dispersion.py:87) ----
     // batches of LB items per thread, all loads of a batch in flight together
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
 
 template <class T>
 void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
-                        cudaStream_t st, const StageMaps *M);
+                        cudaStream_t st, const StageMaps *M, int row0, int nrows);
 
 // fp64 runs the tiled variant (bsq_stage_tiled.cu: 64 registers, 32 warps per
 // SM) -- the column walk needs 128 fp64 registers and loses on latency hiding
@@ -355,9 +355,12 @@ void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<
 // tiled 0.821 vs 0.722 ms).  Measured A/B on B200, round 1.
 template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
-                  cudaStream_t st, const StageMaps *M) {
+                  cudaStream_t st, const StageMaps *M, int row0, int nrows) {
+    static_assert(STAGE_BAND % STY == 0 && STAGE_BAND % STAGE_TY == 0, "band of whole tiles");
+    if (nrows < 0) nrows = C.L.ny - row0;
+    if (nrows <= 0) return;
     if constexpr (sizeof(T) == 8) {
-        launch_stage_tiled(C, P, A, predict, st, M);
+        launch_stage_tiled(C, P, A, predict, st, M, row0, nrows);
     } else {
         const size_t smem = sizeof(StageSmem<T>);
         static bool attr_set = false;
@@ -366,18 +369,20 @@ void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A,
                                  (int)smem);
             attr_set = true;
         }
-        dim3 grid((C.L.nx + SW_ - 1) / SW_, (C.L.ny + STY - 1) / STY);
-        k_stage<T><<<grid, SW_ * SNW, smem, st>>>(C, P, A, predict);
+        dim3 grid((C.L.nx + SW_ - 1) / SW_, (nrows + STY - 1) / STY);
+        k_stage<T><<<grid, SW_ * SNW, smem, st>>>(C, P, A, predict, row0);
     }
 }
 
 #if BSQ_INST_F64
 template void launch_stage<double>(const Consts<double> &, const DevParams *,
-                                   const StagePtrs<double> &, int, cudaStream_t, const StageMaps *);
+                                   const StagePtrs<double> &, int, cudaStream_t, const StageMaps *,
+                                   int, int);
 #endif
 #if BSQ_INST_F32
 template void launch_stage<float>(const Consts<float> &, const DevParams *,
-                                  const StagePtrs<float> &, int, cudaStream_t, const StageMaps *);
+                                  const StagePtrs<float> &, int, cudaStream_t, const StageMaps *,
+                                  int, int);
 #endif
 
 }  // namespace bsq

@@ -75,7 +75,7 @@ struct StageSmem {
 template <class T>
 __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const DevParams *__restrict__ P,
                                                  StagePtrs<T> A, int predict,
-                                                 const __grid_constant__ StageMaps M) {
+                                                 const __grid_constant__ StageMaps M, int row0) {
     // the TMA destinations need 128-B alignment: the kernel has no static
     // smem, so the dynamic window starts at the CTA's smem base (checked)
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     const Layout L = C.L;
     const int nx = L.nx, ny = L.ny;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
-    const int I0 = GL + blockIdx.x * TX, J0 = GL + blockIdx.y * TY;
+    const int I0 = GL + blockIdx.x * TX, J0 = GL + row0 + blockIdx.y * TY;
 
     // ---- A: tile + halo, by TMA ------------------------------------------------
     // One thread issues seven 2-D bulk tensor copies (w, P, Q, bed_eff, depth
@@ -332,26 +332,26 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
 
 template <class T>
 void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
-                        cudaStream_t st, const StageMaps *M) {
+                        cudaStream_t st, const StageMaps *M, int row0, int nrows) {
     const size_t smem = sizeof(tiled::StageSmem<T>);
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(tiled::k_stage<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    dim3 grid((C.L.nx + tiled::TX - 1) / tiled::TX, (C.L.ny + tiled::TY - 1) / tiled::TY);
-    tiled::k_stage<T><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, A, predict, *M);
+    dim3 grid((C.L.nx + tiled::TX - 1) / tiled::TX, (nrows + tiled::TY - 1) / tiled::TY);
+    tiled::k_stage<T><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, A, predict, *M, row0);
 }
 
 #if BSQ_INST_F64
 template void launch_stage_tiled<double>(const Consts<double> &, const DevParams *,
                                          const StagePtrs<double> &, int, cudaStream_t,
-                                         const StageMaps *);
+                                         const StageMaps *, int, int);
 #endif
 #if BSQ_INST_F32
 template void launch_stage_tiled<float>(const Consts<float> &, const DevParams *,
                                         const StagePtrs<float> &, int, cudaStream_t,
-                                        const StageMaps *);
+                                        const StageMaps *, int, int);
 #endif
 
 }  // namespace bsq

@@ -107,7 +107,12 @@ class LocalComm:
     def any_flag(self, flags: list) -> bool:
         return any(flags)
 
-    def halo(self, strips, ids, nrows: int, stream):
+    def halo(self, strips, ids, nrows: int, stream, inner=None):
+        """Copy ``nrows`` boundary rows of arrays ``ids`` between neighbouring
+        strips; ``inner()`` queues the work that reads no halo row (it runs
+        while the transfers are in flight under DistComm)."""
+        if inner is not None:
+            inner()
         with torch.cuda.stream(stream):
             for r in range(self.world - 1):
                 lo, up = strips[r], strips[r + 1]
@@ -190,8 +195,10 @@ class DistComm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return bool(t.item())
 
-    def _exchange(self, send_up, send_dn, recv_up, recv_dn):
-        """Post the four transfers with the neighbours (None = no neighbour)."""
+    def _exchange(self, send_up, send_dn, recv_up, recv_dn, inner=None):
+        """Post the four transfers with the neighbours (None = no neighbour),
+        queue ``inner()`` on the current stream while they are in flight, then
+        make the current stream wait for them."""
         d, r, ops = self.dist, self.rank, []
         if send_up is not None:
             ops.append(d.P2POp(d.isend, send_up, r + 1, group=self.group))
@@ -199,11 +206,13 @@ class DistComm:
         if send_dn is not None:
             ops.append(d.P2POp(d.isend, send_dn, r - 1, group=self.group))
             ops.append(d.P2POp(d.irecv, recv_dn, r - 1, group=self.group))
-        if ops:
-            for w in d.batch_isend_irecv(ops):
-                w.wait()
+        works = d.batch_isend_irecv(ops) if ops else []
+        if inner is not None:
+            inner()  # interior rows: overlap the transfers
+        for w in works:
+            w.wait()
 
-    def halo(self, strips, ids, nrows: int, stream):
+    def halo(self, strips, ids, nrows: int, stream, inner=None):
         s = strips[self.rank]
         n = s.ny
         up, dn = self.rank + 1 < self.world, self.rank > 0
@@ -213,7 +222,7 @@ class DistComm:
             send_dn = torch.cat([v[GHOST:GHOST + nrows] for v in views]) if dn else None
             recv_up = torch.empty_like(send_up) if up else None
             recv_dn = torch.empty_like(send_dn) if dn else None
-            self._exchange(send_up, send_dn, recv_up, recv_dn)
+            self._exchange(send_up, send_dn, recv_up, recv_dn, inner)
             for k, v in enumerate(views):
                 if up:
                     v[n + GHOST:n + GHOST + nrows].copy_(recv_up[k * nrows:(k + 1) * nrows])
@@ -518,13 +527,16 @@ class ShardedDevice:
         sp = {r: self._strip_params(params, r) for r in order}
         for r in order:
             strips[r].phase(nat.PH_GHOST, sp[r])
-        self.comm.halo(strips, _STATE, 2, self.stream)
-        for r in order:
-            strips[r].phase(nat.PH_STAGE)
+
+        def each(ph):
+            return lambda: [strips[r].phase(ph) for r in order]
+        # the stage's and the correction's interior rows run while the halo
+        # rows they do not read are in flight
+        self.comm.halo(strips, _STATE, 2, self.stream, inner=each(nat.PH_STAGE_INNER))
+        each(nat.PH_STAGE_EDGE)()
         self._ysolve(1)
-        self.comm.halo(strips, _PENDING_PQ, 1, self.stream)
-        for r in order:
-            strips[r].phase(nat.PH_CORRECT)
+        self.comm.halo(strips, _PENDING_PQ, 1, self.stream, inner=each(nat.PH_CORRECT_INNER))
+        each(nat.PH_CORRECT_EDGE)()
         self._ysolve(2)
         parts = []
         for r in order:

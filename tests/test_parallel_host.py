@@ -79,7 +79,14 @@ def _worker(rank, port, out_q):
         ranges = split_rows(NY, WORLD)
         strips = {rank: FakeStrip(rank, *ranges[rank])}
         comm = DistComm()
-        comm.halo(strips, (nat.ARR_W, nat.ARR_P, nat.ARR_Q), 2, None)
+        # inner(): the interior work queued while the halo is in flight; it
+        # must see the halo rows before the exchange (snapshot of one ghost row)
+        seen = []
+        s0 = strips[rank]
+
+        def inner():
+            seen.append(s0.f[nat.ARR_W][1].clone())
+        comm.halo(strips, (nat.ARR_W, nat.ARR_P, nat.ARR_Q), 2, None, inner=inner)
         comm.halo(strips, (nat.ARR_P_NEW, nat.ARR_Q_NEW), 1, None)
         comm.pipeline(strips, nat.PH_SOLVE1F, nat.PH_SOLVE1B, None)
         # reductions of per-strip step results
@@ -109,7 +116,8 @@ def _worker(rank, port, out_q):
         table = comm.gather_spike_table({rank: _spike_coef(rank)}, NX)
         yb = comm.spike_bounds(strips, nat.ARR_Q_NEW, None)[rank].numpy().copy()
         out_q.put((rank, {a: t.numpy().copy() for a, t in s.f.items()}, s.col.numpy().copy(),
-                   red, [a.copy() for a in full], got_tail, any_flag, table, yb))
+                   red, [a.copy() for a in full], got_tail, any_flag, table, yb,
+                   [t.numpy() for t in seen]))
     finally:
         dist.destroy_process_group()
 
@@ -187,6 +195,18 @@ def test_distcomm_spike_exchange_matches_localcomm(dist_results):
         table, yb = dist_results[r][6], dist_results[r][7]
         assert np.array_equal(table, want_tab)
         assert np.array_equal(yb, want_yb)
+
+
+def test_distcomm_halo_runs_inner_work_before_the_rows_land(dist_results):
+    """halo(..., inner=f) calls f once, after posting the transfers and
+    before the received rows are written (rank 1's south ghost row 1 still
+    holds its initial value inside f, and the neighbour's row afterwards)."""
+    ranges = split_rows(NY, WORLD)
+    init = FakeStrip(1, *ranges[1]).f[nat.ARR_W][1].numpy()
+    seen = dist_results[1][8]
+    assert len(seen) == 1 and np.array_equal(seen[0], init)
+    assert not np.array_equal(dist_results[1][0][nat.ARR_W][1], init)
+    assert len(dist_results[0][8]) == 1
 
 
 def test_combine_matches_reference_semantics():
