@@ -1143,13 +1143,13 @@ struct Engine : EngineBase {
             // (applied at t+dt before the solves); the queued stage needs the
             // ones at t_{n+1}: save, apply, run, restore
             pre("start");
+            // ghosts at t_{n+1}, saving the frame they overwrite on the way
             ++step_launches;
-            launch_frame(C, W(nxt), Pp(nxt), Qq(nxt), frame_buf(), 1, st);
+            launch_ghost(C, pn, 0, W(nxt), Pp(nxt), Qq(nxt), W(nxt), Pp(nxt), Qq(nxt), st,
+                         frame_buf());
             CU(cudaEventRecord(ev_frame, st));
             frame_w = W(nxt), frame_p = Pp(nxt), frame_q = Qq(nxt);
             frame_restored = false;
-            ++step_launches;
-            launch_ghost(C, pn, 0, W(nxt), Pp(nxt), Qq(nxt), W(nxt), Pp(nxt), Qq(nxt), st);
             pre("ghost_t");
             ++step_launches;
             const StageMaps sm = stage_maps_for(W(nxt), Pp(nxt), Qq(nxt));

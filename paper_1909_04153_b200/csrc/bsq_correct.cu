@@ -21,11 +21,11 @@ template <class T>
 __host__ __device__ constexpr int cr_rows() { return sizeof(T) == 8 ? 2 : BSQ_CORRECT_CR32; }
 
 template <class T>
-__global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K, int row0) {
+__global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) {
     constexpr int CR = cr_rows<T>();
     const Layout L = C.L;
     const int I = GL + blockIdx.x * 32 + threadIdx.x;
-    const int J0 = GL + row0 + (blockIdx.y * 8 + threadIdx.y) * CR;
+    const int J0 = GL + (blockIdx.y * 8 + threadIdx.y) * CR;
     const long pitch = L.pitch;
     if (I >= L.nx + GL || J0 >= L.ny + GL) return;
     T d[CR], dx_[CR], dy_[CR], bu[CR], bv[CR], fs[CR], gs[CR], qw[CR + 2][3], pw[CR + 2][3];
@@ -78,6 +78,8 @@ __global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K, 
 // ---------------------------------------------------------------------------
 // launchers
 
+// A row band runs as a grid of nrows rows whose arrays start row0 rows down
+// (same kernel, no extra operand: an extra parameter cost 10 registers)
 template <class T>
 void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st, int row0,
                     int nrows) {
@@ -85,8 +87,18 @@ void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st
     static_assert(STAGE_BAND % (8 * CR) == 0, "band of whole blocks");
     if (nrows < 0) nrows = C.L.ny - row0;
     if (nrows <= 0) return;
+    Consts<T> Cb = C;
+    CorrectPtrs<T> Kb = K;
+    if (row0 > 0) {
+        const long sh = (long)row0 * C.L.pitch;
+        Cb.L.ny = nrows;
+        Kb.bu += sh, Kb.bv += sh, Kb.fs += sh, Kb.gs += sh, Kb.p1 += sh, Kb.q1 += sh;
+        Kb.dep += sh, Kb.ddx += sh, Kb.ddy += sh, Kb.us += sh, Kb.vs += sh;
+    } else {
+        Cb.L.ny = nrows;
+    }
     dim3 grid((C.L.nx + 31) / 32, (nrows + 8 * CR - 1) / (8 * CR));  // 32 x (8*CR) cells
-    k_correct<T><<<grid, dim3(32, 8), 0, st>>>(C, K, row0);
+    k_correct<T><<<grid, dim3(32, 8), 0, st>>>(Cb, Kb);
 }
 
 #if BSQ_INST_F64

@@ -46,13 +46,27 @@ __device__ __forceinline__ T ns_value(const Consts<T> &C, const DevParams *P, in
 // compose the N/S rule at the mirror column, so no ordering between threads
 // is needed.  src_w/src_p/src_q give the interior the mirrors read (for the
 // t+dt fill: predicted w, old P/Q -- stepper.py:252-254).
+// index of ghost cell (J, I) in k_frame's buffer (rows 0, 1, ny+2, ny+3 over
+// the padded width, then columns 0, 1, nx+2, nx+3 over the interior rows)
+__device__ __forceinline__ long frame_index(int nx, int ny, int J, int I) {
+    const int W = nx + 4;
+    if (J < GL || J >= ny + GL) return (long)(J < GL ? J : J - ny) * W + I;
+    return 4L * W + (long)(I < GL ? I : I - nx) * ny + (J - GL);
+}
+
 template <class T>
 __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which, const T *src_w,
-                        const T *src_p, const T *src_q, T *dst_w, T *dst_p, T *dst_q) {
+                        const T *src_p, const T *src_q, T *dst_w, T *dst_p, T *dst_q, T *save) {
     const int nx = C.L.nx, ny = C.L.ny, nxt = nx + 4, nyt = ny + 4;
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     const T *src[3] = {src_w, src_p, src_q};
     T *dst[3] = {dst_w, dst_p, dst_q};
+    const long nframe = 4L * nxt + 4L * ny;
+    // the frame save: every frame cell is written by exactly one thread, which
+    // reads its old value first
+    auto keep = [&](int f, int J, int I) {
+        if (save) save[f * nframe + frame_index(nx, ny, J, I)] = dst[f][C.L.at(J, I)];
+    };
     if (k < 4 * nyt) {
         int J = k >> 2;
         int c = k & 3;  // 0,1 -> west cols 0,1; 2,3 -> east cols nxt-2, nxt-1
@@ -64,6 +78,7 @@ __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which,
         if (C.side_kind[side] == KIND_MAKER) {
             double gw = which ? P->gw_n[side] : P->gw_t[side];
             double gf = which ? P->gf_n[side] : P->gf_t[side];
+            for (int f = 0; f < 3; f++) keep(f, J, I);
             dst_w[C.L.at(J, I)] = T(gw);
             dst_p[C.L.at(J, I)] = side == SIDE_W ? T(gf) : T(-gf);
             dst_q[C.L.at(J, I)] = T(0);
@@ -74,6 +89,7 @@ __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which,
         for (int f = 0; f < 3; f++) {
             T cur = interior_row ? src[f][C.L.at(J, Im)] : ns_value(C, P, which, f, J, Im, src[f]);
             T s = f == 1 ? T(-1) : T(1);  // P is the wall-normal flux on E/W
+            keep(f, J, I);
             dst[f][C.L.at(J, I)] = s * cur;
         }
         return;
@@ -85,7 +101,10 @@ __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which,
         int J = r < 2 ? r : nyt - 4 + r;
         if (C.side_kind[J < GL ? SIDE_S : SIDE_N] == KIND_INTERNAL) return;
 #pragma unroll
-        for (int f = 0; f < 3; f++) dst[f][C.L.at(J, I)] = ns_value(C, P, which, f, J, I, src[f]);
+        for (int f = 0; f < 3; f++) {
+            keep(f, J, I);
+            dst[f][C.L.at(J, I)] = ns_value(C, P, which, f, J, I, src[f]);
+        }
     }
 }
 
@@ -141,20 +160,20 @@ template void launch_frame<float>(const Consts<float> &, float *, float *, float
 
 template <class T>
 void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
-                  const T *sq, T *dw, T *dp, T *dq, cudaStream_t st) {
+                  const T *sq, T *dw, T *dp, T *dq, cudaStream_t st, T *save) {
     int n = 4 * (C.L.ny + 4) + 4 * C.L.nx;
-    k_ghost<T><<<(n + 127) / 128, 128, 0, st>>>(C, P, which, sw, sp, sq, dw, dp, dq);
+    k_ghost<T><<<(n + 127) / 128, 128, 0, st>>>(C, P, which, sw, sp, sq, dw, dp, dq, save);
 }
 
 #if BSQ_INST_F64
 template void launch_ghost<double>(const Consts<double> &, const DevParams *, int, const double *,
                                    const double *, const double *, double *, double *, double *,
-                                   cudaStream_t);
+                                   cudaStream_t, double *);
 #endif
 #if BSQ_INST_F32
 template void launch_ghost<float>(const Consts<float> &, const DevParams *, int, const float *,
                                   const float *, const float *, float *, float *, float *,
-                                  cudaStream_t);
+                                  cudaStream_t, float *);
 #endif
 
 }  // namespace bsq

@@ -80,9 +80,11 @@ struct FinalPtrs {
     DevParams *pnext;               // speculation: the next step's ghost/stage parameters
 };
 
+// save != nullptr: each ghost cell's previous value goes to save first, in
+// k_frame's layout (the frame save fused into the fill)
 template <class T>
 void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
-                  const T *sq, T *dw, T *dp, T *dq, cudaStream_t st);
+                  const T *sq, T *dw, T *dp, T *dq, cudaStream_t st, T *save = nullptr);
 // stage tile (fp64 tiled kernel): STAGE_TX x STAGE_TY cells per CTA
 #ifndef BSQ_STAGE_TY
 #define BSQ_STAGE_TY 8
