@@ -15,9 +15,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     > $OUT/${TAG}_ncu_l.log 2>&1
 echo "launch list rc=$?"
 # one AB3 step with speculation: skip the initial extrema, step 1 (ghost_t,
-# stage, ghost_n, solve1, correct, solve2, final + the queued frame, ghost_t,
-# stage = 10) and steps 2-3 (8 each), then capture step 4's 8 launches
-# (ghost_n .. final, and the queued frame, ghost_t, stage of step 5)
-ncu --set full --clock-control none --import-source on -s 27 -c 8 \
+# stage, ghost_n, solve1, correct, solve2, final + the queued ghost_t (with the
+# frame save) and stage = 9) and steps 2-3 (7 each), then capture step 4's 7
+# launches (ghost_n .. final, and the queued ghost_t, stage of step 5)
+ncu --set full --clock-control none --import-source on -s 24 -c 7 \
     -o $OUT/${TAG} -f python tools/profile_step.py --steps 2 > $OUT/${TAG}_ncu.log 2>&1
 echo "full rc=$?"
