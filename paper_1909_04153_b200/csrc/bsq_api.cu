@@ -244,6 +244,7 @@ struct Engine : EngineBase {
     bool g_fresh = false;   // g_com holds the committed state's values
     T *maxw = nullptr;      // padded layout, interior used
     bool fold_req = false;  // fold the committed state into maxw at the next stage
+    bool spike_fix_pending = false;  // k_final applies the second solve's spike correction
     // strips: rows [lo, hi) of the stage / the correction read no halo row, so
     // they run while the halo is in flight (BSQ_PH_*_INNER), the rest after
     bool stage_inner = false, correct_inner = false;
@@ -509,8 +510,11 @@ struct Engine : EngineBase {
         if ((solve != 1 && solve != 2) || !ybound) return fail(BSQ_ERR_BAD_ARG, "bad spike_fix args");
         T *x = Qq(1 - cur);  // both solves land in the pending Q
         T *bt = (T *)(base + offs[A_COUNT + S_SPBT]);
+        // the second solve's correction is applied by k_final as it loads Q
+        // (same operations as k_spike_fix, one pass over the strip less)
         launch_spike(C, sp_G, sp_rank, d_sptab, (const T *)ybound, bt, x, arr[A_SPV], arr[A_SPW],
-                     d.south_internal, d.north_internal, st);
+                     d.south_internal, d.north_internal, st, solve == 1);
+        spike_fix_pending = solve == 2;
         CU(cudaGetLastError());
         return BSQ_OK;
     }
@@ -1116,6 +1120,12 @@ struct Engine : EngineBase {
         F.goff = d_goff;
         F.ng = ng;
         F.gval = d_gval;
+        F.spbt = spike_fix_pending ? (const T *)(base + offs[A_COUNT + S_SPBT]) : nullptr;
+        F.spv = arr[A_SPV];
+        F.spw = arr[A_SPW];
+        F.sp_south = d.south_internal;
+        F.sp_north = d.north_internal;
+        spike_fix_pending = false;
         const bool spec = hparams->spec && !strip() && !fold_req;
         F.P = dparams;
         F.pnext = spec ? dpar[pk ^ 1] : nullptr;

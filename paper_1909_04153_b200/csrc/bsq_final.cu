@@ -217,7 +217,7 @@ static __device__ void spec_next(const DevParams &P, double max_rate, DevParams 
 }
 
 
-template <class T>
+template <class T, bool SPIKE>
 __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, FinalPtrs<T> F) {
     __shared__ bool am_last;
     const Layout L = C.L;
@@ -241,6 +241,17 @@ __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, Final
             vw[k] = F.w[o];
             vp[k] = F.pin[o];
             vq[k] = F.qin[o];
+        }
+        if (SPIKE) {  // the strip's coupling correction of the second solve (k_spike_fix)
+#pragma unroll
+            for (int k = 0; k < FG; k++) {
+                const bool in = iin && J0 + (k0 + k) * FY < ny + GL;
+                const long o = in ? o0 + (k0 + k) * rstep : L.at(GL, GL);
+                T r = vq[k];
+                if (F.sp_south) r = r - F.spv[o] * F.spbt[I - GL];
+                if (F.sp_north) r = r - F.spw[o] * F.spbt[nx + I - GL];
+                vq[k] = r;
+            }
         }
 #pragma unroll
         for (int k = 0; k < FG; k++) {
@@ -277,7 +288,7 @@ __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, Final
             // compared, so a zero's sign is kept exactly)
             if (bits(w) != bits(vw[k])) F.w[o] = w;
             if (F.pout != F.pin || bits(p) != bits(vp[k])) F.pout[o] = p;
-            if (F.qout != F.qin || bits(q) != bits(vq[k])) F.qout[o] = q;
+            if (SPIKE || F.qout != F.qin || bits(q) != bits(vq[k])) F.qout[o] = q;
             T dv = w - rest;  // blow-up deviation (stepper.py:295)
             dv = dv < T(0) ? -dv : dv;
             if (dv != dv) r.nan = 1;
@@ -401,7 +412,10 @@ int final_blocks(int nx, int ny) {
 
 template <class T>
 void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st) {
-    k_final<T><<<final_grid(C.L.nx, C.L.ny), dim3(FX, FY), 0, st>>>(C, F);
+    if (F.spbt)
+        k_final<T, true><<<final_grid(C.L.nx, C.L.ny), dim3(FX, FY), 0, st>>>(C, F);
+    else
+        k_final<T, false><<<final_grid(C.L.nx, C.L.ny), dim3(FX, FY), 0, st>>>(C, F);
 }
 
 template <class T>

@@ -78,6 +78,10 @@ struct FinalPtrs {
     T *gval;                        // ng x (w, P, Q) of the new state
     const DevParams *P;             // this step's parameters (controller inputs)
     DevParams *pnext;               // speculation: the next step's ghost/stage parameters
+    // BSQ_Y_SPIKE: the second solve's coupling correction, applied on load
+    // (q - v b_prev - w t_next, k_spike_fix's operations) instead of a pass
+    const T *spv, *spw, *spbt;      // null: no correction pending
+    int sp_south, sp_north;
 };
 
 // save != nullptr: each ghost cell's previous value goes to save first, in
@@ -126,9 +130,11 @@ void launch_extrema(const Consts<T> &C, const T *w, const T *p, const T *q, cons
                     Partial *part, cudaStream_t st);
 int final_blocks(int nx, int ny);
 // BSQ_Y_SPIKE: per-column coupling system + in-place correction of a strip's Q
+// apply = 0: only the per-column coupling values bt (k_final applies them)
 template <class T>
 void launch_spike(const Consts<T> &C, int G, int rank, const double *table, const T *yb, T *bt,
-                  T *x, const T *v, const T *w, int south, int north, cudaStream_t st);
+                  T *x, const T *v, const T *w, int south, int north, cudaStream_t st,
+                  int apply = 1);
 // observers: gauge gather and the running max of w
 template <class T>
 void launch_gather(const T *w, const T *p, const T *q, const long long *goff, int ng, T *gval,

@@ -92,8 +92,10 @@ __global__ void k_spike_fix(Consts<T> C, T *x, const T *v, const T *w, const T *
 
 template <class T>
 void launch_spike(const Consts<T> &C, int G, int rank, const double *table, const T *yb, T *bt,
-                  T *x, const T *v, const T *w, int south, int north, cudaStream_t st) {
+                  T *x, const T *v, const T *w, int south, int north, cudaStream_t st,
+                  int apply) {
     k_spike_reduce<T><<<(C.L.nx + 127) / 128, 128, 0, st>>>(C.L.nx, G, rank, table, yb, bt);
+    if (!apply) return;
     dim3 blk(32, 8), grd((C.L.nx + 31) / 32, (C.L.ny + 7) / 8);
     k_spike_fix<T><<<grd, blk, 0, st>>>(C, x, v, w, bt, south, north);
 }
@@ -101,12 +103,12 @@ void launch_spike(const Consts<T> &C, int G, int rank, const double *table, cons
 #if BSQ_INST_F64
 template void launch_spike<double>(const Consts<double> &, int, int, const double *,
                                    const double *, double *, double *, const double *,
-                                   const double *, int, int, cudaStream_t);
+                                   const double *, int, int, cudaStream_t, int);
 #endif
 #if BSQ_INST_F32
 template void launch_spike<float>(const Consts<float> &, int, int, const double *, const float *,
                                   float *, float *, const float *, const float *, int, int,
-                                  cudaStream_t);
+                                  cudaStream_t, int);
 #endif
 
 }  // namespace bsq
