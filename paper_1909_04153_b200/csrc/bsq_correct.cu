@@ -17,8 +17,11 @@ namespace bsq {
 #ifndef BSQ_CORRECT_CR32
 #define BSQ_CORRECT_CR32 4
 #endif
+#ifndef BSQ_CORRECT_CR64
+#define BSQ_CORRECT_CR64 2
+#endif
 template <class T>
-__host__ __device__ constexpr int cr_rows() { return sizeof(T) == 8 ? 2 : BSQ_CORRECT_CR32; }
+__host__ __device__ constexpr int cr_rows() { return sizeof(T) == 8 ? BSQ_CORRECT_CR64 : BSQ_CORRECT_CR32; }
 
 template <class T>
 __global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) {
