@@ -143,6 +143,32 @@ def dist_env():
     return rank, world, local
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_cmd(nproc: int, argv: list) -> list:
+    """torchrun command that re-runs this script as ``nproc`` ranks on this
+    node (rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+            f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+
+
+def relaunch(nproc: int) -> int:
+    """``python bench.py --gpus N`` outside torchrun: start the N ranks
+    ourselves (one process per GPU), pass their output through (rank 0
+    prints the JSON line) and return their exit status.  NCCL logs its
+    communicator set-up (nranks) so the run shows every rank joined."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.run(launch_cmd(nproc, sys.argv[1:]), env=env).returncode
+
+
 def cpu_baseline(case, steps: int, threads: int):
     """Time the CPU oracle (C restatement of the reference step) on the
     same case; returns Gcell-updates/s and the wall time."""
@@ -159,8 +185,8 @@ def cpu_baseline(case, steps: int, threads: int):
     return cells * steps / dt / 1e9, dt
 
 
-def config_dict(args, case, world):
-    g = case.bathy.grid
+def config_dict(args, case, world, g=None):
+    g = g or case.bathy.grid
     return {"workload": f"C5 rip channel + JONSWAP maker, 4096x4096 per GPU, global "
                         f"{g.nx}x{g.ny}" + (", y-strips" if world > 1 else ""),
             "nx": g.nx, "ny_per_gpu": g.ny // world, "ny_global": g.ny, "gpus": world,
@@ -171,11 +197,24 @@ def config_dict(args, case, world):
             "l2": "inputs larger than L2 (134 MB per field)"}
 
 
-def run_reference(args, rank):
+def run_reference(args, rank, world=1):
     """CPU reference arm: the oracle (bitwise = reference) on all host cores,
-    on the per-GPU workload (rank 0 only)."""
-    if rank != 0:
+    on the per-GPU workload (rank 0 only; under N ranks the others wait at a
+    gloo barrier and exit without work)."""
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        try:
+            if rank == 0:
+                _run_reference(args)
+            dist.barrier()
+        finally:
+            dist.destroy_process_group()
         return
+    _run_reference(args)
+
+
+def _run_reference(args):
     from oracle import oracle as orc
     from paper_1909_04153_b200.scenario import make_case
     case = make_case("C4", scale=args.scale)
@@ -218,9 +257,14 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=6)  # ~10 s of oracle work at 4096^2
     args = ap.parse_args()
     rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with "
+                         f"--nproc-per-node {args.gpus}, or without torchrun")
 
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, world)
         return
 
     import torch
@@ -235,6 +279,8 @@ def main():
         from paper_1909_04153_b200.parallel import DistComm, ShardedSimulator
         dist = dist_mod
         torch.cuda.set_device(local)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator set-up (nranks) in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist.barrier()  # communicator up on every rank before the first P2P exchange
         comm = DistComm()
@@ -243,8 +289,16 @@ def main():
     clocks = ClockSampler(dev.index)
     clocks.start()
 
-    case = make_case("C5", gpus=world, scale=args.scale)
-    cells_total = case.bathy.grid.nx * case.bathy.grid.ny
+    if world > 1:
+        # each rank builds only its own strip of the global grid (bitwise the
+        # global build's rows; the two global scalars by all-reduce)
+        from paper_1909_04153_b200.scenario import make_strip_case
+        case = make_strip_case("C5", rank, world, reduce=comm.reduce_scalar, scale=args.scale)
+        gg = case.grid
+    else:
+        case = make_case("C5", gpus=1, scale=args.scale)
+        gg = case.bathy.grid
+    cells_total = gg.nx * gg.ny
     cells_gpu = cells_total // world
 
     def make_sim(precision="fp64", state=None):
@@ -255,7 +309,7 @@ def main():
             # SPIKE-coupled column solves: ranks run concurrently (the bitwise
             # rank pipeline serializes the y sweeps over ranks)
             return ShardedSimulator(case.bathy, st, case.boundaries, ctrl, comm=comm,
-                                    coupling="spike", **kw)
+                                    coupling="spike", global_grid=gg, **kw)
         return stepper.Simulator(case.bathy, st, case.boundaries, ctrl, **kw)
 
     def max_over_ranks(x: float) -> float:
@@ -350,10 +404,7 @@ def main():
     pin_out = [torch.empty(a.shape, dtype=torch.float64).pin_memory().numpy() for a in pin]
     # both pinned buffers have been used once before the timed region (the
     # constructor uploaded from pin): bring the state back into pin_out once
-    if world > 1:
-        sim._dev.download_local(out=pin_out)
-    else:
-        sim.download_state(out=pin_out)
+    sim.download_state(out=pin_out)
     barrier()
     t0 = time.perf_counter()
     sim.state = FieldState(*pin)  # upload (a rank uploads its strip)
@@ -361,13 +412,10 @@ def main():
     for _ in range(args.steps):
         sim.advance()
     t_st = time.perf_counter()
-    if world > 1:
-        sim._dev.download_local(out=pin_out)  # each rank brings back its own strip
-    else:
-        sim.download_state(out=pin_out)
+    sim.download_state(out=pin_out)  # a rank brings back its own strip
     t_dn = time.perf_counter()
     e2e_s = max_over_ranks(t_dn - t0)
-    state_bytes = 3 * 8 * (cells_gpu + 4 * case.bathy.grid.nx)
+    state_bytes = 3 * 8 * (cells_gpu + 4 * gg.nx)
     h2d = state_bytes / args.steps + ctypes.sizeof(nat.StepParams)
     d2h = state_bytes / args.steps + ctypes.sizeof(nat.StepResult)
     e2e = {"value": cells_total * args.steps / e2e_s / 1e9, "unit": "Gcell-updates/s",
@@ -394,7 +442,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (rip-channel bathymetry, JONSWAP maker; reference generators)",
-            "config": config_dict(args, case, world), "roofline": roofline, "cpu_baseline": cpu,
+            "config": config_dict(args, case, world, gg), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": kps * args.steps, "clocks": clock_info, "fp32": fp32,
         }
         print(json.dumps(line), flush=True)

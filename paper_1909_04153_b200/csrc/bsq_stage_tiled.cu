@@ -28,6 +28,9 @@
 
 namespace bsq {
 
+#ifndef BSQ_STAGE_MAP2D
+#define BSQ_STAGE_MAP2D 1  // warp-per-row item maps for the face / flux phases
+#endif
 #ifndef BSQ_STAGE_MINB
 #define BSQ_STAGE_MINB 4  // CTAs per SM the register budget is sized for (64 regs)
 #endif
@@ -57,6 +60,13 @@ struct StageSmem {
     alignas(128) T bfx[TY][BFXW];    // bed_face_x for columns -2..TX
     alignas(128) T bfy[TY + 3][TX];  // bed_face_y for rows -2..TY
     alignas(8) uint64_t bar;
+#if BSQ_STAGE_MAP2D
+    struct {  // phase B/C faces (hi = east/north, lo = west/south; w, P, Q);
+              // phase C/D fluxes over the hi faces (flux v in hi array v)
+        T xhi[3][TY][FXW], xlo[3][TY][FXW];
+        T yhi[3][FYH][TX], ylo[3][FYH][TX];
+    } f;
+#else
     union {
         struct {  // phase B/C: faces (hi = east/north, lo = west/south)
             T xwhi[TY][FXW], xwlo[TY][FXW], xphi[TY][FXW], xplo[TY][FXW], xqhi[TY][FXW],
@@ -69,6 +79,7 @@ struct StageSmem {
             T fy[3][TY + 1][TX];
         } x;
     } u;
+#endif
 };
 
 
@@ -127,6 +138,86 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         }
     }
     mbar_wait(&S.bar, 0);
+#if BSQ_STAGE_MAP2D
+    // ---- B: faces, once per cell, + eta -----------------------------------------
+    // Warp ty, lane tx (2-D map: no div/mod, no warp covering two kinds):
+    //   round 0  x faces of tile row ty, face columns 0..31
+    //   round 1  y faces of face row ty (0..7)
+    //   round 2  warps 0,1: y face rows 8, 9; warp 2: x face columns 32, 33 of
+    //            the 8 rows (16 lanes); warps 3..7: eta over the halo box
+    auto xface = [&](int r, int c) {  // x faces of cell (row r, column c-1)
+        const int y = r + 2, x = c + 1;
+        const Faces<T> f = cell_faces(S.w[y][x - 1], S.w[y][x], S.w[y][x + 1], S.p[y][x - 1],
+                                      S.p[y][x], S.p[y][x + 1], S.q[y][x - 1], S.q[y][x],
+                                      S.q[y][x + 1], S.bfx[r][c + 1], S.bfx[r][c], C.theta);
+        S.f.xhi[0][r][c] = f.whi;
+        S.f.xlo[0][r][c] = f.wlo;
+        S.f.xhi[1][r][c] = f.phi;
+        S.f.xlo[1][r][c] = f.plo;
+        S.f.xhi[2][r][c] = f.qhi;
+        S.f.xlo[2][r][c] = f.qlo;
+    };
+    auto yface = [&](int r, int c) {  // y faces of cell (row r-1, column c)
+        const int y = r + 1, x = c + 2;
+        const Faces<T> f = cell_faces(S.w[y - 1][x], S.w[y][x], S.w[y + 1][x], S.p[y - 1][x],
+                                      S.p[y][x], S.p[y + 1][x], S.q[y - 1][x], S.q[y][x],
+                                      S.q[y + 1][x], S.bfy[r + 1][c], S.bfy[r][c], C.theta);
+        S.f.yhi[0][r][c] = f.whi;
+        S.f.ylo[0][r][c] = f.wlo;
+        S.f.yhi[1][r][c] = f.phi;
+        S.f.ylo[1][r][c] = f.plo;
+        S.f.yhi[2][r][c] = f.qhi;
+        S.f.ylo[2][r][c] = f.qlo;
+    };
+    static_assert(TX == 32 && TY == 8, "2-D item maps assume 32 x 8 tiles (warp = tile row)");
+    xface(ty, tx);
+    yface(ty, tx);
+    if (ty < 2) {
+        yface(TY + ty, tx);
+    } else if (ty == 2) {
+        if (tx < 2 * TY) xface(tx >> 1, TX + (tx & 1));
+    } else {
+        // eta = (w - bed_eff) - depth over the halo box (dispersion.py:87)
+        for (int k = tid - 3 * TX; k < HY * HX; k += NT - 3 * TX)
+            (&S.eta[0][0])[k] = ((&S.w[0][0])[k] - (&S.be[0][0])[k]) - (&S.dep[0][0])[k];
+    }
+    __syncthreads();
+
+    // ---- C: fluxes, written over the faces they consume --------------------------
+    //   round 0  x interfaces of row ty, 0..31;  round 1  y interface row ty
+    //   round 2  warp 0: y interface row 8; warp 1: x interface 32 of the 8 rows
+    // Interface (r, xi) reads the east ("hi") faces of column xi and the west
+    // ("lo") faces of column xi+1.  Column xi's hi faces feed no other
+    // interface, so the thread that consumed them stores the three fluxes in
+    // their place (flux v -> hi array v): no barrier and no registers held
+    // between computing and storing.  Same for y with row yi's north faces.
+    auto xflux = [&](int r, int xi) {
+        T f1, f2, f3;
+        cu_flux_rcp(S.f.xhi[0][r][xi], S.f.xlo[0][r][xi + 1], S.f.xhi[1][r][xi],
+                    S.f.xlo[1][r][xi + 1], S.f.xhi[2][r][xi], S.f.xlo[2][r][xi + 1],
+                    S.bfx[r][xi + 1], C.g, C.h_eps, f1, f2, f3);
+        S.f.xhi[0][r][xi] = f1;
+        S.f.xhi[1][r][xi] = f2;
+        S.f.xhi[2][r][xi] = f3;
+    };
+    auto yflux = [&](int yi, int c) {  // south cell = face row yi; normal = Q
+        T f1, fq, fp;
+        cu_flux_rcp(S.f.yhi[0][yi][c], S.f.ylo[0][yi + 1][c], S.f.yhi[2][yi][c],
+                    S.f.ylo[2][yi + 1][c], S.f.yhi[1][yi][c], S.f.ylo[1][yi + 1][c],
+                    S.bfy[yi + 1][c], C.g, C.h_eps, f1, fq, fp);
+        S.f.yhi[0][yi][c] = f1;
+        S.f.yhi[1][yi][c] = fp;  // fy2 carries P
+        S.f.yhi[2][yi][c] = fq;  // fy3 carries Q
+    };
+    xflux(ty, tx);
+    yflux(ty, tx);
+    if (ty == 0) yflux(TY, tx);
+    else if (ty == 1 && tx < TY) xflux(tx, TX);
+    __syncthreads();
+    // phase D's view of the fluxes
+#define FX(v, r, xi) S.f.xhi[v][r][xi]
+#define FY(v, yi, c) S.f.yhi[v][yi][c]
+#else
     // eta = (w - bed_eff) - depth over the halo box (dispersion.py:87)
     for (int k = tid; k < HY * HX; k += NT) {
         (&S.eta[0][0])[k] = ((&S.w[0][0])[k] - (&S.be[0][0])[k]) - (&S.dep[0][0])[k];
@@ -206,6 +297,9 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         }
     }
     __syncthreads();
+#define FX(v, r, xi) S.u.x.fx[v][r][xi]
+#define FY(v, yi, c) S.u.x.fy[v][yi][c]
+#endif
 
     // ---- D: per cell ----------------------------------------------------------------
     const int J = J0 + ty, I = I0 + tx;
@@ -218,8 +312,8 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     const T bn_ = S.bfy[ty + 2][tx], bs_ = S.bfy[ty + 1][tx];
 
     // fv_rates (_kernels.py:230-251)
-    T rw = -(S.u.x.fx[0][ty][tx + 1] - S.u.x.fx[0][ty][tx]) * C.inv_dx -
-           (S.u.x.fy[0][ty + 1][tx] - S.u.x.fy[0][ty][tx]) * C.inv_dy;
+    T rw = -(FX(0, ty, tx + 1) - FX(0, ty, tx)) * C.inv_dx -
+           (FY(0, ty + 1, tx) - FY(0, ty, tx)) * C.inv_dy;
     const T src_x = -C.g * (wc - T(0.5) * (be_ + bw_)) * (be_ - bw_) * C.inv_dx;
     const T src_y = -C.g * (wc - T(0.5) * (bn_ + bs_)) * (bn_ - bs_) * C.inv_dy;
     T h = wc - S.be[y][x];
@@ -230,10 +324,10 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         const T h2 = hstar * hstar;
         fric = div_rcp(C.c_f * sqrt(pc * pc + qc * qc), h2, rcp_rn(h2));
     }
-    T rp = -(S.u.x.fx[1][ty][tx + 1] - S.u.x.fx[1][ty][tx]) * C.inv_dx -
-           (S.u.x.fy[1][ty + 1][tx] - S.u.x.fy[1][ty][tx]) * C.inv_dy + src_x - fric * pc;
-    T rq = -(S.u.x.fx[2][ty][tx + 1] - S.u.x.fx[2][ty][tx]) * C.inv_dx -
-           (S.u.x.fy[2][ty + 1][tx] - S.u.x.fy[2][ty][tx]) * C.inv_dy + src_y - fric * qc;
+    T rp = -(FX(1, ty, tx + 1) - FX(1, ty, tx)) * C.inv_dx -
+           (FY(1, ty + 1, tx) - FY(1, ty, tx)) * C.inv_dy + src_x - fric * pc;
+    T rq = -(FX(2, ty, tx + 1) - FX(2, ty, tx)) * C.inv_dx -
+           (FY(2, ty + 1, tx) - FY(2, ty, tx)) * C.inv_dy + src_y - fric * qc;
 
     const T d = S.dep[y][x], dx_ = A.ddx[o], dy_ = A.ddy[o];
     T fs_, gs_;

@@ -133,6 +133,52 @@ def build_bathymetry(grid: Grid, bed_interior, ws: float,
                       bed_face_x=fx, bed_face_y=fy, h_eps=float(h_eps))
 
 
+def build_bathymetry_rows(grid: Grid, bed_rows, row0: int, ny: int, ws: float,
+                          h_eps: float) -> Bathymetry:
+    """The static fields of padded rows [row0, row0 + ny + 4) of the grid --
+    one y-strip of ``build_bathymetry(grid, bed, ws, h_eps)`` -- computed from
+    bed rows only: ``bed_rows(j0, j1)`` returns interior bed rows [j0, j1)
+    (clipped to the grid).  Every value is the one the whole-grid call makes:
+    the 3-cell symmetric pad is applied at the global edges only, the corner /
+    face / cell means are the same elementwise expressions, and the y slope
+    uses central differences inside the grid and np.gradient's one-sided ones
+    at its edges (one extra depth row each side makes the strip's rows
+    central).  ``h_eps`` must be the whole grid's (it depends on the global
+    maximum depth).  The returned Bathymetry's grid is the strip's own
+    (``ny`` rows starting at ``y0 + row0 * dy``); bed_face_y has ny + 3 rows."""
+    G3 = GHOST + 1
+    # ext rows [e0, e1) of the 3-padded bed (global ext row e is bed row e - 3,
+    # reflected symmetrically at the grid edges like np.pad 'symmetric'):
+    # enough for cell rows row0 - 1 .. row0 + ny + 4 and face rows of the strip
+    e0, e1 = row0 - 1, row0 + ny + 2 * GHOST + 3
+    e0c, e1c = max(e0, 0), min(e1, grid.ny + 2 * G3)
+    src = np.arange(e0c, e1c) - G3
+    src = np.where(src < 0, -src - 1, src)
+    src = np.where(src >= grid.ny, 2 * grid.ny - 1 - src, src)
+    lo, hi = int(src.min()), int(src.max()) + 1
+    b = np.asarray(bed_rows(lo, hi), dtype=np.float64)
+    if b.shape != (hi - lo, grid.nx):
+        raise ValueError(f"bed rows shape {b.shape}, expected {(hi - lo, grid.nx)}")
+    if not np.all(np.isfinite(b)):
+        raise ValueError("bed contains non-finite values")
+    ext = np.pad(b[src - lo], ((0, 0), (G3, G3)), mode="symmetric")
+    sw, nw_, se, ne = ext[:-1, :-1], ext[1:, :-1], ext[:-1, 1:], ext[1:, 1:]
+    corner = 0.25 * ((sw + nw_) + (se + ne))            # rows e0c .. e1c - 2
+    fx = 0.5 * (corner[:-1, 1:-1] + corner[1:, 1:-1])
+    fy = 0.5 * (corner[1:-1, :-1] + corner[1:-1, 1:])   # rows e0c .. e1c - 3
+    eff = 0.25 * ((corner[:-1, :-1] + corner[1:, :-1])
+                  + (corner[:-1, 1:] + corner[1:, 1:]))  # padded rows e0c .. e1c - 3
+    depth = np.maximum(ws - eff, 0.0)
+    ddy, ddx = np.gradient(depth, grid.dy, grid.dx)
+    k = row0 - e0c  # padded row row0 within the computed blocks
+    n = ny + 2 * GHOST
+    sg = Grid(grid.nx, ny, grid.dx, grid.dy, grid.x0, grid.y0 + row0 * grid.dy)
+    return Bathymetry(grid=sg, ws=float(ws), bed=ext[k + 1:k + 1 + n, 1:-1].copy(),
+                      bed_eff=eff[k:k + n].copy(), depth=depth[k:k + n].copy(),
+                      depth_dx=ddx[k:k + n].copy(), depth_dy=ddy[k:k + n].copy(),
+                      bed_face_x=fx[k:k + n].copy(), bed_face_y=fy[k:k + n - 1].copy(), h_eps=float(h_eps))
+
+
 @dataclass
 class FieldState:
     """Surface elevation w and volume fluxes P (x) and Q (y), padded

@@ -39,6 +39,7 @@ import torch
 from . import _native as nat
 from .device import DeviceStep
 from .grid import GHOST
+from . import boundary as bc
 from .stepper import Simulator
 
 _N, _S = 0, 1  # side indices (bsq.h order N, S, E, W)
@@ -106,6 +107,9 @@ class LocalComm:
 
     def any_flag(self, flags: list) -> bool:
         return any(flags)
+
+    def max_scalar(self, x: float) -> float:
+        return x
 
     def halo(self, strips, ids, nrows: int, stream, inner=None):
         """Copy ``nrows`` boundary rows of arrays ``ids`` between neighbouring
@@ -194,6 +198,16 @@ class DistComm:
         t = torch.tensor([1 if any(flags) else 0], dtype=torch.int64, device=self._dev())
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return bool(t.item())
+
+    def reduce_scalar(self, x: float, op: str) -> float:
+        """All-reduce of one float64 ("max" or "min"); exact (no rounding)."""
+        t = torch.tensor([x], dtype=torch.float64, device=self._dev())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.MIN,
+                             group=self.group)
+        return float(t.item())
+
+    def max_scalar(self, x: float) -> float:
+        return self.reduce_scalar(x, "max")
 
     def _exchange(self, send_up, send_dn, recv_up, recv_dn, inner=None):
         """Post the four transfers with the neighbours (None = no neighbour),
@@ -385,10 +399,12 @@ class ShardedDevice:
     """Drop-in for DeviceStep over y-strips (the Simulator drives it)."""
 
     def __init__(self, sim: "ShardedSimulator", desc, bathy, device, world: int, comm,
-                 coupling: str = "pipeline"):
+                 coupling: str = "pipeline", local_inputs: bool = False):
         if coupling not in ("pipeline", "spike"):
             raise ValueError(f"coupling must be 'pipeline' or 'spike', got {coupling!r}")
         self.sim, self.comm, self.world = sim, comm, world
+        # local_inputs: bathy / state arrays are this process's strip only
+        self.local_inputs = local_inputs
         self.spike = coupling == "spike" and world > 1
         self.nx, self.ny = desc.nx, desc.ny
         self.shape = (desc.ny + 2 * GHOST, desc.nx + 2 * GHOST)
@@ -419,7 +435,8 @@ class ShardedDevice:
             # the pipelined recurrence continues the south strip's factorization;
             # spike blocks are factored alone
             cws = comm.get_tail(tails, r, desc.nx) if r > 0 and not self.spike else None
-            strip = DeviceStep(d, _StripStatic(bathy, row0, n), device=dev, stream=self.stream,
+            strip = DeviceStep(d, _StripStatic(bathy, 0 if local_inputs else row0, n), device=dev,
+                               stream=self.stream,
                                cw_south=cws)
             self.strips[r] = strip
             if not self.spike:
@@ -437,13 +454,24 @@ class ShardedDevice:
         self._res = nat.StepResult()
 
     # -- state -----------------------------------------------------------------------
+    def _rows(self, r):
+        row0, n = self.ranges[r]
+        return slice(0 if self.local_inputs else row0, (0 if self.local_inputs else row0) + n + 2 * GHOST)
+
     def upload(self, w, p, q):
         for r, s in self.strips.items():
-            row0, n = self.ranges[r]
-            rows = slice(row0, row0 + n + 2 * GHOST)
+            rows = self._rows(r)
             s.upload(w[rows], p[rows], q[rows])
 
     def download(self, pending: bool = False, out=None):
+        if self.local_inputs:  # this process's strip, in the strip's own shape
+            (s,) = self.strips.values()
+            full = s.download(pending=pending)
+            if out is not None:
+                for dst, src in zip(out, full):
+                    dst[...] = src
+                return out
+            return full
         per = {r: s.download(pending=pending) for r, s in self.strips.items()}
         full = self.comm.gather_state(per, self.shape, self.ranges)
         if out is not None:
@@ -456,8 +484,7 @@ class ShardedDevice:
         """Copy only this process's strips into the matching rows of the
         global arrays ``out`` (w, p, q): the distributed-I/O path."""
         for r, s in self.strips.items():
-            row0, n = self.ranges[r]
-            rows = slice(row0, row0 + n + 2 * GHOST)
+            rows = self._rows(r)
             w, p, q = s.download()
             out[0][rows], out[1][rows], out[2][rows] = w, p, q
         return out
@@ -601,21 +628,54 @@ class ShardedSimulator(Simulator):
     bitwise-checkable against the single-GPU run), or ``comm=DistComm()``
     under torchrun with one strip per process.  Inputs are the global
     objects; every API is the Simulator's.
+
+    ``global_grid`` (DistComm only): the inputs are this rank's strip instead
+    -- ``bathy``/``state`` hold padded rows [row0, row0 + ny_r + 4) of the
+    global arrays (scenario.make_strip_case; bathy.grid is the strip's grid)
+    and ``global_grid`` is the whole grid, so no rank ever holds global
+    arrays.  ``state`` and the downloads are then this rank's strip; the
+    blow-up bound uses the global initial amplitude (one all-reduce).
     """
 
     def __init__(self, *args, world: int | None = None, comm=None, coupling: str = "pipeline",
-                 **kw):
+                 global_grid=None, **kw):
         if comm is None:
             comm = LocalComm(world or 1)
+        if global_grid is not None and len(comm.local) != 1:
+            raise ValueError("strip-local inputs need one strip per process (DistComm)")
         self._comm = comm
         self._world = comm.world
         self._coupling = coupling
+        self._global_grid = global_grid
         super().__init__(*args, **kw)
 
     def _make_device(self, desc, bathy, device):
         if self.solver != "thomas":
             raise NotImplementedError("sharded solves use the Thomas pipeline")
-        return ShardedDevice(self, desc, bathy, device, self._world, self._comm, self._coupling)
+        return ShardedDevice(self, desc, bathy, device, self._world, self._comm, self._coupling,
+                             local_inputs=self._global_grid is not None)
+
+    def _validate_inputs(self, state, bathy, boundaries):
+        if self._global_grid is None:
+            return super()._validate_inputs(state, bathy, boundaries)
+        row0, n = split_rows(self._global_grid.ny, self._world)[self._comm.rank]
+        g = bathy.grid
+        if (g.nx, g.ny) != (self._global_grid.nx, n):
+            raise ValueError(f"strip grid {g.nx}x{g.ny} is not rank {self._comm.rank}'s "
+                             f"{self._global_grid.nx}x{n} rows of the global grid")
+        # a side facing another strip has no boundary policy to validate
+        sides = {s: getattr(boundaries, s) for s in bc.SIDES}
+        if row0 > 0:
+            sides["south"] = bc.Wall()
+        if row0 + n < self._global_grid.ny:
+            sides["north"] = bc.Wall()
+        super()._validate_inputs(state, bathy, bc.Boundaries(**sides))
+
+    def _desc_grid(self, grid):
+        return self._global_grid if self._global_grid is not None else grid
+
+    def _global_max(self, x: float) -> float:
+        return self._comm.max_scalar(x) if self._global_grid is not None else x
 
     @property
     def stream(self):

@@ -8,6 +8,7 @@ assembles the named configs used by tests and bench.py.
 
 from __future__ import annotations
 
+import dataclasses
 import math
 import warnings
 from dataclasses import dataclass
@@ -15,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import boundary as bc
-from .grid import GHOST, Grid, PhysParams, build_bathymetry, still_state
+from .grid import GHOST, Grid, PhysParams, build_bathymetry, build_bathymetry_rows, still_state
 
 
 @dataclass(frozen=True)
@@ -62,12 +63,19 @@ def solitary_wave_ic(spec: SolitaryWaveSpec, bathy, g: float = 9.81):
     return state
 
 
-def rip_channel_bathymetry(grid: Grid, h_eps=None):
-    """Plane beach with a rip channel (reference scenario.py:57-72, paper Eq. 48)."""
-    xc, yc = np.meshgrid(grid.x_centers(), grid.y_centers())
+def rip_channel_bed(grid: Grid, j0: int = 0, j1: int | None = None) -> np.ndarray:
+    """Interior bed rows [j0, j1) of the rip-channel beach (reference
+    scenario.py:57-72, paper Eq. 48): the same elementwise expression on the
+    same cell centres, so any row range is bitwise the whole grid's rows."""
+    xc, yc = np.meshgrid(grid.x_centers(), grid.y_centers()[j0:j1])
     reach = (18.0 - xc) / 30.0
     bump = 3.0 * np.exp(-(18.0 - xc) / 3.0) * np.cos(np.pi * yc / 30.0) ** 10
-    return build_bathymetry(grid, 0.1 - reach * (1.0 + bump), ws=0.0, h_eps=h_eps)
+    return 0.1 - reach * (1.0 + bump)
+
+
+def rip_channel_bathymetry(grid: Grid, h_eps=None):
+    """Plane beach with a rip channel (reference scenario.py:57-72, paper Eq. 48)."""
+    return build_bathymetry(grid, rip_channel_bed(grid), ws=0.0, h_eps=h_eps)
 
 
 def berkhoff_bed(grid: Grid, ws: float = 0.0) -> np.ndarray:
@@ -128,13 +136,55 @@ def make_case(name: str, gpus: int = 1, scale: int = 1) -> Case:
                                north=bc.Sponge(1.0, 10.0))
         return Case(name, bathy, still_state(bathy), bounds, PhysParams(), 0.002)
     if name in ("C4", "C5"):
-        n = 4096 // scale
-        ny = n * (gpus if name == "C5" else 1)
-        grid = Grid(n, ny, 20.48 / n, 30.0 / n, x0=0.0, y0=-15.0)
+        grid = rip_grid(name, gpus, scale)
         bathy = rip_channel_bathymetry(grid)
         d_west = float(bathy.depth[GHOST:-GHOST, GHOST].min())
-        comps = bc.jonswap_components(bc.SpectrumSpec(0.13, 1.6, 68, 0.01, 7), d_west)
-        bounds = bc.Boundaries(west=bc.IrregularMaker(tuple(comps)), east=bc.Wall(),
-                               south=bc.Wall(), north=bc.Wall())
-        return Case(name, bathy, still_state(bathy), bounds, PhysParams(c_f=0.0025), 0.001)
+        return Case(name, bathy, still_state(bathy), _rip_bounds(d_west),
+                    PhysParams(c_f=0.0025), 0.001)
     raise ValueError(f"unknown case {name!r}")
+
+
+def rip_grid(name: str, gpus: int = 1, scale: int = 1) -> Grid:
+    """The C4 (4096^2) / C5 (4096 x 4096*gpus) rip-channel grid."""
+    n = 4096 // scale
+    ny = n * (gpus if name == "C5" else 1)
+    return Grid(n, ny, 20.48 / n, 30.0 / n, x0=0.0, y0=-15.0)
+
+
+def _rip_bounds(d_west: float):
+    comps = bc.jonswap_components(bc.SpectrumSpec(0.13, 1.6, 68, 0.01, 7), d_west)
+    return bc.Boundaries(west=bc.IrregularMaker(tuple(comps)), east=bc.Wall(),
+                         south=bc.Wall(), north=bc.Wall())
+
+
+@dataclass
+class StripCase(Case):
+    """One rank's y-strip of a case: ``bathy``/``state`` hold padded rows
+    [row0, row0 + ny + 4) of the global arrays; ``grid`` is the global grid."""
+
+    grid: Grid | None = None
+    row0: int = 0
+
+
+def make_strip_case(name: str, rank: int, world: int, reduce=None, scale: int = 1) -> StripCase:
+    """Rank ``rank``'s strip of C4 / C5 split over ``world`` y-strips
+    (parallel.split_rows), built from its own rows only -- no rank holds the
+    global grid.  The two global scalars the whole-grid build derives (h_eps
+    from the maximum depth, the maker's west depth from a column minimum) come
+    through ``reduce(value, "max" | "min")`` (an all-reduce across ranks; None:
+    single process, the values of this strip).  Bitwise the rows of
+    ``make_case(name, world, scale)`` (tests/test_parallel_host.py)."""
+    from .parallel import split_rows
+    if name not in ("C4", "C5"):
+        raise ValueError(f"strip-local build supports C4 / C5, not {name!r}")
+    reduce = reduce or (lambda v, op: v)
+    grid = rip_grid(name, world, scale)
+    row0, ny = split_rows(grid.ny, world)[rank]
+    bathy = build_bathymetry_rows(grid, lambda a, b: rip_channel_bed(grid, a, b), row0, ny,
+                                  ws=0.0, h_eps=1.0)
+    # build_bathymetry: h_eps = 1e-6 * max(1, depth.max()) over every padded row
+    h_eps = 1e-6 * max(1.0, float(reduce(float(bathy.depth.max()), "max")))
+    bathy = dataclasses.replace(bathy, h_eps=h_eps)
+    d_west = float(reduce(float(bathy.depth[GHOST:-GHOST, GHOST].min()), "min"))
+    return StripCase(name, bathy, still_state(bathy), _rip_bounds(d_west),
+                     PhysParams(c_f=0.0025), 0.001, grid=grid, row0=row0)

@@ -190,9 +190,8 @@ class Simulator:
         self.h_dry = h_dry if h_dry is not None else 100.0 * bathy.h_eps
         if self.h_dry < 0.0:
             raise ValueError("h_dry must be non-negative")
-        _validate_state(state, bathy)
-        bc.validate_boundaries(boundaries, bathy)
-        grid = bathy.grid
+        self._validate_inputs(state, bathy, boundaries)
+        grid = self._desc_grid(bathy.grid)
         self._policies = [getattr(boundaries, s) for s in bc.SIDES]
         self._kinds = [bc.policy_kind(p) for p in self._policies]
         self._warn_dominance()
@@ -227,8 +226,8 @@ class Simulator:
         self.history = DeviceHistory(self._dev)
         self.records: list[StepRecord] = []
         self._rest = np.maximum(bathy.ws, bathy.bed_eff)
-        ii = grid.interior
-        amp0 = float(np.max(np.abs(state.w[ii] - self._rest[ii])))
+        ii = bathy.grid.interior
+        amp0 = self._global_max(float(np.max(np.abs(state.w[ii] - self._rest[ii]))))
         self.initial_amplitude = amp0
         self.blowup_bound = blowup_bound if blowup_bound is not None else 10.0 * amp0 + 1.0
         self.clamped_volume = 0.0
@@ -259,6 +258,18 @@ class Simulator:
     def _make_device(self, desc, bathy, device):
         """The device engine for the whole grid (ShardedSimulator overrides)."""
         return DeviceStep(desc, bathy, device=device)
+
+    # hooks a strip-local ShardedSimulator overrides (its inputs are one y-strip)
+    def _validate_inputs(self, state, bathy, boundaries):
+        _validate_state(state, bathy)
+        bc.validate_boundaries(boundaries, bathy)
+
+    def _desc_grid(self, grid):
+        """The grid the device descriptor and the sponge bands describe."""
+        return grid
+
+    def _global_max(self, x: float) -> float:
+        return x
 
     # -- implicit operator (host copy, for inspection and the warning) ----------
     def _warn_dominance(self):
