@@ -12,13 +12,17 @@
 // and writes the new stage level, the predicted w, U*, V* and the
 // quadrature bases.  Faces and fluxes live only in shared memory.
 //
-// CTA = 32 x 8 cells.  Phases (each ends in __syncthreads):
-//   A  load w, P, Q (+ eta) for the tile and a 2-cell halo, and face beds
+// CTA = 32 x 8 cells, warp ty = tile row ty.  Three CTA barriers:
+//   A  load w, P, Q, bed_eff, depth for the tile and a 2-cell halo, and the
+//      face beds, by TMA (one mbarrier)
 //   B  faces of every cell once: x faces for columns -1..32, y faces for
-//      rows -1..8 of the tile (the reference evaluates each face once too)
-//   C  fluxes of the 33 x 8 x-interfaces and 32 x 9 y-interfaces, held in
-//      registers across a barrier and stored over the dead face buffers
+//      rows -1..8 of the tile (the reference evaluates each face once too),
+//      eta over the halo box                                     | barrier
+//   C  fluxes of the 33 x 8 x-interfaces and 32 x 9 y-interfaces, each
+//      stored over the east/north faces it alone consumed         | barrier
 //   D  per-cell rates, dispersive terms, cross groups, U*/V*, predictor
+// Phases B and C map items to (warp, lane) directly -- row ty, column lane --
+// in three rounds, so no warp mixes item kinds and no index needs a divide.
 #include <cmath>
 #include <cstdint>
 
@@ -28,9 +32,6 @@
 
 namespace bsq {
 
-#ifndef BSQ_STAGE_MAP2D
-#define BSQ_STAGE_MAP2D 1  // warp-per-row item maps for the face / flux phases
-#endif
 #ifndef BSQ_STAGE_MINB
 #define BSQ_STAGE_MINB 4  // CTAs per SM the register budget is sized for (64 regs)
 #endif
@@ -60,30 +61,15 @@ struct StageSmem {
     alignas(128) T bfx[TY][BFXW];    // bed_face_x for columns -2..TX
     alignas(128) T bfy[TY + 3][TX];  // bed_face_y for rows -2..TY
     alignas(8) uint64_t bar;
-#if BSQ_STAGE_MAP2D
     struct {  // phase B/C faces (hi = east/north, lo = west/south; w, P, Q);
               // phase C/D fluxes over the hi faces (flux v in hi array v)
         T xhi[3][TY][FXW], xlo[3][TY][FXW];
         T yhi[3][FYH][TX], ylo[3][FYH][TX];
     } f;
-#else
-    union {
-        struct {  // phase B/C: faces (hi = east/north, lo = west/south)
-            T xwhi[TY][FXW], xwlo[TY][FXW], xphi[TY][FXW], xplo[TY][FXW], xqhi[TY][FXW],
-                xqlo[TY][FXW];
-            T ywhi[FYH][TX], ywlo[FYH][TX], yphi[FYH][TX], yplo[FYH][TX], yqhi[FYH][TX],
-                yqlo[FYH][TX];
-        } f;
-        struct {  // phase C/D: fluxes through the tile's interfaces
-            T fx[3][TY][TX + 1];
-            T fy[3][TY + 1][TX];
-        } x;
-    } u;
-#endif
 };
 
 
-template <class T>
+template <class T, bool FR>
 __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const DevParams *__restrict__ P,
                                                  StagePtrs<T> A, int predict,
                                                  const __grid_constant__ StageMaps M, int row0) {
@@ -122,23 +108,18 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     // phase D's per-cell inputs that phase A does not read: start them towards
     // L2 now (no registers held), so phase D's loads hit on chip
     {
-        const int Jc = J0 + ty, Ic = I0 + tx;
-        // one lane per 128-B line (16 doubles) issues the prefetch
-        if ((tx & (128 / sizeof(T) - 1)) == 0 && Jc < ny + GL && Ic < nx + GL) {
-            const long oc = L.at(Jc, Ic);
-            prefetch_l2(A.ddx + oc);
-            prefetch_l2(A.ddy + oc);
-            if (predict && !P->euler) {
-#pragma unroll
-                for (int f = 0; f < 5; f++) {
-                    prefetch_l2(A.h1[f] + oc);
-                    prefetch_l2(A.h2[f] + oc);
-                }
-            }
+        // lane k < 24 of warp ty: array k >> 1 (ddx, ddy, h1[0..4], h2[0..4]),
+        // 128-B line k & 1 of the warp's 256-B tile row
+        constexpr int LINE = 128 / sizeof(T);
+        const int Jc = J0 + ty, Ic = I0 + (tx & 1) * LINE;
+        const int na = (predict && !P->euler) ? 12 : 2;
+        if (tx < 2 * na && Jc < ny + GL && Ic < nx + GL) {
+            const int k = tx >> 1;
+            const T *base = k == 0 ? A.ddx : k == 1 ? A.ddy : k < 7 ? A.h1[k - 2] : A.h2[k - 7];
+            prefetch_l2(base + L.at(Jc, Ic));
         }
     }
     mbar_wait(&S.bar, 0);
-#if BSQ_STAGE_MAP2D
     // ---- B: faces, once per cell, + eta -----------------------------------------
     // Warp ty, lane tx (2-D map: no div/mod, no warp covering two kinds):
     //   round 0  x faces of tile row ty, face columns 0..31
@@ -193,7 +174,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     // between computing and storing.  Same for y with row yi's north faces.
     auto xflux = [&](int r, int xi) {
         T f1, f2, f3;
-        cu_flux_rcp(S.f.xhi[0][r][xi], S.f.xlo[0][r][xi + 1], S.f.xhi[1][r][xi],
+        cu_flux_rcp<FR>(S.f.xhi[0][r][xi], S.f.xlo[0][r][xi + 1], S.f.xhi[1][r][xi],
                     S.f.xlo[1][r][xi + 1], S.f.xhi[2][r][xi], S.f.xlo[2][r][xi + 1],
                     S.bfx[r][xi + 1], C.g, C.h_eps, f1, f2, f3);
         S.f.xhi[0][r][xi] = f1;
@@ -202,7 +183,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     };
     auto yflux = [&](int yi, int c) {  // south cell = face row yi; normal = Q
         T f1, fq, fp;
-        cu_flux_rcp(S.f.yhi[0][yi][c], S.f.ylo[0][yi + 1][c], S.f.yhi[2][yi][c],
+        cu_flux_rcp<FR>(S.f.yhi[0][yi][c], S.f.ylo[0][yi + 1][c], S.f.yhi[2][yi][c],
                     S.f.ylo[2][yi + 1][c], S.f.yhi[1][yi][c], S.f.ylo[1][yi + 1][c],
                     S.bfy[yi + 1][c], C.g, C.h_eps, f1, fq, fp);
         S.f.yhi[0][yi][c] = f1;
@@ -217,89 +198,6 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     // phase D's view of the fluxes
 #define FX(v, r, xi) S.f.xhi[v][r][xi]
 #define FY(v, yi, c) S.f.yhi[v][yi][c]
-#else
-    // eta = (w - bed_eff) - depth over the halo box (dispersion.py:87)
-    for (int k = tid; k < HY * HX; k += NT) {
-        (&S.eta[0][0])[k] = ((&S.w[0][0])[k] - (&S.be[0][0])[k]) - (&S.dep[0][0])[k];
-    }
-    __syncthreads();
-
-    // ---- B: faces, once per cell ------------------------------------------------
-    for (int k = tid; k < NXF + NYF; k += NT) {
-        if (k < NXF) {  // x faces of cell (row r, column c-1), c = 0..TX+1
-            const int r = k / FXW, c = k - r * FXW;
-            const int y = r + 2, x = c + 1;  // smem coords of the cell
-            const Faces<T> f = cell_faces(S.w[y][x - 1], S.w[y][x], S.w[y][x + 1], S.p[y][x - 1],
-                                          S.p[y][x], S.p[y][x + 1], S.q[y][x - 1], S.q[y][x],
-                                          S.q[y][x + 1], S.bfx[r][c + 1], S.bfx[r][c], C.theta);
-            S.u.f.xwhi[r][c] = f.whi;
-            S.u.f.xwlo[r][c] = f.wlo;
-            S.u.f.xphi[r][c] = f.phi;
-            S.u.f.xplo[r][c] = f.plo;
-            S.u.f.xqhi[r][c] = f.qhi;
-            S.u.f.xqlo[r][c] = f.qlo;
-        } else {  // y faces of cell (row r-1, column c), r = 0..TY+1
-            const int kk = k - NXF;
-            const int r = kk / TX, c = kk - r * TX;
-            const int y = r + 1, x = c + 2;
-            const Faces<T> f = cell_faces(S.w[y - 1][x], S.w[y][x], S.w[y + 1][x], S.p[y - 1][x],
-                                          S.p[y][x], S.p[y + 1][x], S.q[y - 1][x], S.q[y][x],
-                                          S.q[y + 1][x], S.bfy[r + 1][c], S.bfy[r][c], C.theta);
-            S.u.f.ywhi[r][c] = f.whi;
-            S.u.f.ywlo[r][c] = f.wlo;
-            S.u.f.yphi[r][c] = f.phi;
-            S.u.f.yplo[r][c] = f.plo;
-            S.u.f.yqhi[r][c] = f.qhi;
-            S.u.f.yqlo[r][c] = f.qlo;
-        }
-    }
-    __syncthreads();
-
-    // ---- C: fluxes (registers across the barrier, then over the faces) ----------
-    T fl[FL_PASSES][3];
-#pragma unroll
-    for (int s = 0; s < FL_PASSES; s++) {
-        const int k = tid + s * NT;
-        if (k < NXI) {  // interface between tile columns xi-1 and xi, row r
-            const int r = k / (TX + 1), xi = k - r * (TX + 1);
-            // left cell = face column xi, right cell = face column xi+1
-            cu_flux_rcp(S.u.f.xwhi[r][xi], S.u.f.xwlo[r][xi + 1], S.u.f.xphi[r][xi],
-                        S.u.f.xplo[r][xi + 1], S.u.f.xqhi[r][xi], S.u.f.xqlo[r][xi + 1],
-                        S.bfx[r][xi + 1], C.g, C.h_eps, fl[s][0], fl[s][1], fl[s][2]);
-        } else if (k < NFL) {  // interface between tile rows yi-1 and yi, column c
-            const int kk = k - NXI;
-            const int yi = kk / TX, c = kk - yi * TX;
-            // south cell = face row yi, north cell = face row yi+1; normal = Q
-            T f1, fq, fp;
-            cu_flux_rcp(S.u.f.ywhi[yi][c], S.u.f.ywlo[yi + 1][c], S.u.f.yqhi[yi][c],
-                        S.u.f.yqlo[yi + 1][c], S.u.f.yphi[yi][c], S.u.f.yplo[yi + 1][c],
-                        S.bfy[yi + 1][c], C.g, C.h_eps, f1, fq, fp);
-            fl[s][0] = f1;
-            fl[s][1] = fp;  // fy2 carries P
-            fl[s][2] = fq;  // fy3 carries Q
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < FL_PASSES; s++) {
-        const int k = tid + s * NT;
-        if (k < NXI) {
-            const int r = k / (TX + 1), xi = k - r * (TX + 1);
-            S.u.x.fx[0][r][xi] = fl[s][0];
-            S.u.x.fx[1][r][xi] = fl[s][1];
-            S.u.x.fx[2][r][xi] = fl[s][2];
-        } else if (k < NFL) {
-            const int kk = k - NXI;
-            const int yi = kk / TX, c = kk - yi * TX;
-            S.u.x.fy[0][yi][c] = fl[s][0];
-            S.u.x.fy[1][yi][c] = fl[s][1];
-            S.u.x.fy[2][yi][c] = fl[s][2];
-        }
-    }
-    __syncthreads();
-#define FX(v, r, xi) S.u.x.fx[v][r][xi]
-#define FY(v, yi, c) S.u.x.fy[v][yi][c]
-#endif
 
     // ---- D: per cell ----------------------------------------------------------------
     const int J = J0 + ty, I = I0 + tx;
@@ -424,17 +322,28 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
 
 }  // namespace tiled
 
-template <class T>
-void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
-                        cudaStream_t st, const StageMaps *M, int row0, int nrows) {
+template <class T, bool FR>
+static void launch_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
+                         cudaStream_t st, const StageMaps *M, int row0, int nrows) {
     const size_t smem = sizeof(tiled::StageSmem<T>);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(tiled::k_stage<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(tiled::k_stage<T, FR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
         attr_set = true;
     }
     dim3 grid((C.L.nx + tiled::TX - 1) / tiled::TX, (nrows + tiled::TY - 1) / tiled::TY);
-    tiled::k_stage<T><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, A, predict, *M, row0);
+    tiled::k_stage<T, FR><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, A, predict, *M,
+                                                                         row0);
+}
+
+template <class T>
+void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
+                        cudaStream_t st, const StageMaps *M, int row0, int nrows) {
+    if (flux_fast_rcp_ok(C.h_eps))
+        launch_tiled<T, true>(C, P, A, predict, st, M, row0, nrows);
+    else
+        launch_tiled<T, false>(C, P, A, predict, st, M, row0, nrows);
 }
 
 #if BSQ_INST_F64
