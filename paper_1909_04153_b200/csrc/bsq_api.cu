@@ -95,7 +95,9 @@ size_t layout_bytes(const bsq_desc *d, size_t offs[A_COUNT + S_COUNT], int *fac_
     *fac_stride = fs;
     const size_t small[S_COUNT] = {sizeof(T) * d->ny, sizeof(T) * d->nx, sizeof(T) * 4 * fs,
                                    sizeof(DevParams), sizeof(DevResult),
-                                   sizeof(Partial) * (size_t)final_blocks(d->nx, d->ny), 256,
+                                   sizeof(Partial) * (size_t)(final_blocks(d->nx, d->ny) +
+                                                              final_rows(d->nx, d->ny)),
+                                   sizeof(unsigned int) * (size_t)(1 + final_rows(d->nx, d->ny)),
                                    sizeof(T) * d->nx, sizeof(T) * d->nx, sizeof(T) * d->nx,
                                    sizeof(T) * d->nx, sizeof(T) * 2 * d->nx, sizeof(DevParams),
                                    sizeof(T) * frame_elems(d->nx, d->ny)};
@@ -662,7 +664,7 @@ struct Engine : EngineBase {
             (rc = upload_padded(arr[A_BFY], f->bed_face_y, ny + 3, nx + 4)) ||
             (rc = factor_lines(f)) || (rc = build_maps()))
             return rc;
-        CU(cudaMemsetAsync(counter, 0, sizeof(unsigned int), st));
+        CU(cudaMemsetAsync(counter, 0, sizeof(unsigned int) * (1 + final_rows(nx, ny)), st));
         CU(cudaStreamSynchronize(st));
         return BSQ_OK;
     }

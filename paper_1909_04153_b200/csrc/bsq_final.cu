@@ -123,7 +123,7 @@ __device__ __forceinline__ Red red_block(Red r) {
 
 // speed_extrema contribution of one cell (_kernels.py:337-352); the serial
 // scan's `if x > max` skips NaN, hence the !(x > 0) guards.
-template <class T>
+template <bool FAST = false, class T>
 __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, T be, Acc<T> &r) {
     // a dry, still cell (h = 0, P = Q = 0) contributes rate = speed = depth = 0,
     // which never raises a maximum: skip it (whole dry warps branch over)
@@ -132,7 +132,9 @@ __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, 
     h = floor0(h);
     const T hstar = floor_eps(h, C.h_eps);
     const T c = sqrt(C.g * h);
-    const T nrh = -rcp_rn(hstar);  // both quotients correctly rounded via one reciprocal
+    // both quotients correctly rounded via one reciprocal (branch-free when
+    // h_eps is in rcp_rn_inrange's range: bsq_device.cuh flux_fast_rcp_ok)
+    const T nrh = -(FAST ? rcp_depth(hstar) : rcp_rn(hstar));
     const T su = div_nonneg(fabs(p), hstar, nrh) + c;
     const T sv = div_nonneg(fabs(q), hstar, nrh) + c;
     const T rate = nb_max(su * C.inv_dx, sv * C.inv_dy);
@@ -140,6 +142,35 @@ __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, 
     if (rate > r.rate) r.rate = rate;
     if (speed > r.speed) r.speed = speed;
     if (h > r.depth) r.depth = h;
+}
+
+__device__ __forceinline__ Partial to_partial(const Red &r) {
+    Partial pt;
+    pt.max_rate = r.rate;
+    pt.max_speed = r.speed;
+    pt.max_depth = r.depth;
+    pt.max_dev = r.dev;
+    pt.clamped = r.clamp;
+    pt.dev_nan = r.nan;
+    pt.pad_ = 0;
+    return pt;
+}
+
+// fold n partials written by other CTAs: thread t takes t, t+FT, ... in
+// order, then the block tree; result valid in thread 0
+__device__ __forceinline__ Red fold_partials(const Partial *p, int n) {
+    const int tid = threadIdx.y * FX + threadIdx.x;
+    Red a{0, 0, 0, 0, 0, 0};
+    for (int k = tid; k < n; k += FT) {
+        const Partial *pp = p + k;
+        a.rate = fmax(a.rate, __ldcg(&pp->max_rate));
+        a.speed = fmax(a.speed, __ldcg(&pp->max_speed));
+        a.depth = fmax(a.depth, __ldcg(&pp->max_depth));
+        a.dev = fmax(a.dev, __ldcg(&pp->max_dev));
+        a.clamp = a.clamp + __ldcg(&pp->clamped);
+        a.nan |= __ldcg(&pp->dev_nan);
+    }
+    return red_block(a);
 }
 
 // Python's min / max of two floats: the first argument unless the second is
@@ -217,7 +248,7 @@ static __device__ void spec_next(const DevParams &P, double max_rate, DevParams 
 }
 
 
-template <class T, bool SPIKE>
+template <class T, bool SPIKE, bool FAST>
 __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, FinalPtrs<T> F) {
     __shared__ bool am_last;
     const Layout L = C.L;
@@ -299,41 +330,39 @@ __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, Final
                 if (!isfinite(p)) atomicMin(&F.res->state_bad[1], lin);
                 if (!isfinite(q)) atomicMin(&F.res->state_bad[2], lin);
             }
-            extrema_cell(C, w, p, q, be, r);
+            extrema_cell<FAST>(C, w, p, q, be, r);
         }
     }
     Red rr = red_block_warped(red_warp(r));
     const int tid = threadIdx.y * FX + threadIdx.x;
-    const int nblk = gridDim.x * gridDim.y, bid = blockIdx.y * gridDim.x + blockIdx.x;
+    // Two-level deterministic fold: the last CTA of each grid row folds that
+    // row's partials (in order) into a row partial; the last row folder folds
+    // the row partials (in order).  Each fold is one round of parallel L2
+    // loads (ld.cg: written by other CTAs before their fence + counter
+    // increment) and a block reduction -- no long serial tail.
+    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
+    Partial *rowp = F.part + (size_t)gridDim.x * gridDim.y;  // one per grid row
     if (tid == 0) {
-        Partial pt;
-        pt.max_rate = rr.rate;
-        pt.max_speed = rr.speed;
-        pt.max_depth = rr.depth;
-        pt.max_dev = rr.dev;
-        pt.clamped = rr.clamp;
-        pt.dev_nan = rr.nan;
-        pt.pad_ = 0;
-        F.part[bid] = pt;
+        F.part[bid] = to_partial(rr);
         __threadfence();
-        const unsigned int prev = atomicAdd(F.counter, 1u);
-        am_last = prev == (unsigned int)(nblk - 1);
+        const unsigned int prev = atomicAdd(&F.counter[1 + blockIdx.y], 1u);
+        am_last = prev == gridDim.x - 1;
     }
     __syncthreads();
     if (!am_last) return;
     __threadfence();
-    // last CTA: reduce the partials; thread t folds partials t, t+FT, ... in order
-    Red a{0, 0, 0, 0, 0, 0};
-    for (int k = tid; k < nblk; k += FT) {
-        const volatile Partial *pp = (const volatile Partial *)&F.part[k];
-        a.rate = fmax(a.rate, pp->max_rate);
-        a.speed = fmax(a.speed, pp->max_speed);
-        a.depth = fmax(a.depth, pp->max_depth);
-        a.dev = fmax(a.dev, pp->max_dev);
-        a.clamp = a.clamp + pp->clamped;
-        a.nan |= pp->dev_nan;
+    const Red row = fold_partials(F.part + (size_t)blockIdx.y * gridDim.x, gridDim.x);
+    if (tid == 0) {
+        rowp[blockIdx.y] = to_partial(row);
+        F.counter[1 + blockIdx.y] = 0u;
+        __threadfence();
+        const unsigned int prev = atomicAdd(&F.counter[0], 1u);
+        am_last = prev == gridDim.y - 1;
     }
-    a = red_block(a);
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    const Red a = fold_partials(rowp, gridDim.y);
     // gauge cells of the new state (scenario.py:184-202 reads w, P, Q there);
     // other CTAs wrote them: read through L2
     for (int g = tid; g < F.ng; g += FT) {
@@ -348,7 +377,7 @@ __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, Final
         F.res->max_depth = a.depth;
         F.res->max_dev = a.nan ? (double)NAN : a.dev;
         F.res->clamped = a.clamp;
-        *F.counter = 0u;
+        F.counter[0] = 0u;
         if (F.pnext && F.P->spec) spec_next(*F.P, a.rate, *F.pnext, F.res->next);
     }
 }
@@ -408,14 +437,17 @@ int final_blocks(int nx, int ny) {
     dim3 g = final_grid(nx, ny);
     return (int)(g.x * g.y);
 }
+int final_rows(int nx, int ny) { return (int)final_grid(nx, ny).y; }
 #endif
 
 template <class T>
 void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st) {
+    const dim3 grid = final_grid(C.L.nx, C.L.ny), blk(FX, FY);
+    const bool fast = flux_fast_rcp_ok(C.h_eps);
     if (F.spbt)
-        k_final<T, true><<<final_grid(C.L.nx, C.L.ny), dim3(FX, FY), 0, st>>>(C, F);
+        (fast ? k_final<T, true, true> : k_final<T, true, false>)<<<grid, blk, 0, st>>>(C, F);
     else
-        k_final<T, false><<<final_grid(C.L.nx, C.L.ny), dim3(FX, FY), 0, st>>>(C, F);
+        (fast ? k_final<T, false, true> : k_final<T, false, false>)<<<grid, blk, 0, st>>>(C, F);
 }
 
 template <class T>

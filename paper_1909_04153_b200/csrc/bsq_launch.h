@@ -129,6 +129,7 @@ template <class T>
 void launch_extrema(const Consts<T> &C, const T *w, const T *p, const T *q, const T *be,
                     Partial *part, cudaStream_t st);
 int final_blocks(int nx, int ny);
+int final_rows(int nx, int ny);  // k_final grid rows: row partials + counters
 // BSQ_Y_SPIKE: per-column coupling system + in-place correction of a strip's Q
 // apply = 0: only the per-column coupling values bt (k_final applies them)
 template <class T>

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         S.f.yhi[2][r][c] = f.qhi;
         S.f.ylo[2][r][c] = f.qlo;
     };
-    static_assert(TX == 32 && TY == 8, "2-D item maps assume 32 x 8 tiles (warp = tile row)");
+    static_assert(TX == 32 && TY >= 4 && TY <= 16, "2-D item maps: warp = tile row, 32 columns");
     xface(ty, tx);
     yface(ty, tx);
     if (ty < 2) {
