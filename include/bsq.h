@@ -16,8 +16,12 @@
  *     arrays ny x nx (grid.py:1-20).
  *   - Device memory is owned by the caller: bsq_workspace_bytes() says how
  *     much, bsq_create() carves its buffers out of that one allocation (the
- *     Python host passes a torch-owned CUDA tensor).  The library never
- *     allocates device memory itself.
+ *     Python host passes a torch-owned CUDA tensor).  Outside the workspace
+ *     the library makes only these small or opt-in allocations of its own:
+ *     the step parameter / result blocks and reduction partials, the SPIKE
+ *     table (G x 4 x nx, bsq_set_spike_table), the gauge buffers
+ *     (bsq_set_gauges) and the running-max field (one padded array, only
+ *     after BSQ_MAX_RESET); all are freed by bsq_destroy.
  *   - All device work runs on the stream given to bsq_create (NULL: the
  *     library creates a non-blocking stream).  Calls that return host
  *     results synchronize that stream before returning.
@@ -202,7 +206,8 @@ enum {
     BSQ_ARR_W = 0, BSQ_ARR_P = 1, BSQ_ARR_Q = 2,                /* committed state */
     BSQ_ARR_W_NEW = 3, BSQ_ARR_P_NEW = 4, BSQ_ARR_Q_NEW = 5,    /* pending state */
     BSQ_ARR_DW_IN = 6, BSQ_ARR_DW_OUT = 7, BSQ_ARR_X_IN = 8, BSQ_ARR_X_OUT = 9, /* nx vectors */
-    BSQ_ARR_Q2 = 10                                             /* second-solve Q */
+    BSQ_ARR_Q2 = 10  /* scratch Q of the bsq_solve_momentum seam (the step itself solves
+                        both times into BSQ_ARR_Q_NEW) */
 };
 int bsq_array_layout(bsq_ctx *ctx, int array, size_t *byte_offset, int *pitch, int *xo,
                      int *elem_bytes);
@@ -216,10 +221,13 @@ int bsq_pivot_flags(bsq_ctx *ctx, int *all_positive, int *singular);
  * strip's block against its south / north coupling column) are gathered into
  * a G x 4 x nx table, in rank order, and given to every rank.
  * Per solve (after BSQ_PH_SOLVE1F or BSQ_PH_SOLVE2F): gather every rank's
- * first and last solved row of Q (BSQ_ARR_Q_NEW for solve 1, BSQ_ARR_Q2 for
- * solve 2) into a device array G x 2 x nx of the context's precision, then
- * bsq_spike_fix(solve, ...) solves the coupling system per column and
- * corrects this strip's Q in place, on the library stream. */
+ * first and last solved row of Q (BSQ_ARR_Q_NEW: both solves land in the
+ * pending Q) into a device array G x 2 x nx of the context's precision, then
+ * bsq_spike_fix(solve, ...) solves the coupling system per column.  Solve 1's
+ * correction is applied to Q in place on the library stream.  Solve 2's is
+ * deferred: BSQ_PH_FINAL applies it as k_final loads Q, so the pending Q
+ * is the coupled solution only after BSQ_PH_FINAL (a new BSQ_PH_GHOST drops
+ * a correction that never reached BSQ_PH_FINAL). */
 int bsq_spike_coeffs(bsq_ctx *ctx, double *out);
 int bsq_set_spike_table(bsq_ctx *ctx, const double *table, int nranks, int rank);
 int bsq_spike_fix(bsq_ctx *ctx, int solve, const void *ybound_device);

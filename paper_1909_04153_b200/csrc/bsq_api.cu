@@ -934,6 +934,9 @@ struct Engine : EngineBase {
         case BSQ_PH_GHOST: {
             cur_p = p;
             step_launches = 0;
+            // a step abandoned after bsq_spike_fix(2) (e.g. a failed exchange)
+            // must not hand its coupling correction to this step's k_final
+            spike_fix_pending = false;
             spec_used = !strip() && spec_matches(p);
             spec_pending = false;
             if (spec_used) {  // the stage already ran (on dpar[pk ^ 1])

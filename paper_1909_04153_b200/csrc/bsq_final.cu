@@ -278,9 +278,10 @@ __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, Final
             for (int k = 0; k < FG; k++) {
                 const bool in = iin && J0 + (k0 + k) * FY < ny + GL;
                 const long o = in ? o0 + (k0 + k) * rstep : L.at(GL, GL);
+                const int ic = iin ? I - GL : 0;  // no read past the 2*nx bound rows
                 T r = vq[k];
-                if (F.sp_south) r = r - F.spv[o] * F.spbt[I - GL];
-                if (F.sp_north) r = r - F.spw[o] * F.spbt[nx + I - GL];
+                if (F.sp_south) r = r - F.spv[o] * F.spbt[ic];
+                if (F.sp_north) r = r - F.spw[o] * F.spbt[nx + ic];
                 vq[k] = r;
             }
         }
