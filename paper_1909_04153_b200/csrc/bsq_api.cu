@@ -333,6 +333,7 @@ struct Engine : EngineBase {
         const bsq_desc *p = &d;
         C.L = L;
         C.g = T(p->g);
+        C.half_g = T(0.5) * C.g;
         C.h_eps = T(p->h_eps);
         C.theta = T(p->theta);
         C.c_f = T(p->c_f);
@@ -577,6 +578,28 @@ struct Engine : EngineBase {
             (rc = make_map_box(&smap_bfy, arr[A_BFY], nxt, nyt - 1, TX, TY + 3)))
             return rc;
         return BSQ_OK;
+    }
+    // 32 x 8 tile boxes of the stage's phase-D inputs (static slopes and the
+    // ring slots), built once per array
+    std::vector<std::pair<const T *, CUtensorMap>> pf_cache;
+    const CUtensorMap *pf_map(const T *a) {
+        for (auto &e : pf_cache)
+            if (e.first == a) return &e.second;
+        CUtensorMap m;
+        if (make_map_box(&m, const_cast<T *>(a), d.nx + 4, d.ny + 4, STAGE_TX, STAGE_TY)) return nullptr;
+        pf_cache.emplace_back(a, m);
+        return &pf_cache.back().second;
+    }
+    StageMaps stage_maps_for(const StagePtrs<T> &A) {
+        StageMaps M = stage_maps_for(A.w, A.p, A.q);
+        const T *src[12] = {A.ddx, A.ddy, A.h1[0], A.h1[1], A.h1[2], A.h1[3], A.h1[4],
+                            A.h2[0], A.h2[1], A.h2[2], A.h2[3], A.h2[4]};
+        for (int k = 0; k < 12; k++) {
+            const CUtensorMap *m = src[k] ? pf_map(src[k]) : nullptr;
+            if (m) M.pf[k] = *m;
+            else std::memset(&M.pf[k], 0, sizeof(CUtensorMap));
+        }
+        return M;
     }
     StageMaps stage_maps_for(const T *w, const T *p, const T *q) {
         StageMaps M;
@@ -977,8 +1000,9 @@ struct Engine : EngineBase {
         case BSQ_PH_STAGE:
             if (!spec_used) {
                 ++step_launches;
-                const StageMaps sm = stage_maps_for(W(cur), Pp(cur), Qq(cur));
-                launch_stage(C, dparams, stage_ptrs(slot), 1, st, &sm);
+                const StagePtrs<T> A = stage_ptrs(slot);
+                const StageMaps sm = stage_maps_for(A);
+                launch_stage(C, dparams, A, 1, st, &sm);
                 fold_req = false;
                 ev_mark("stage");
             }
@@ -1019,23 +1043,25 @@ struct Engine : EngineBase {
             stage_inner = !spec_used && hi > lo;
             if (stage_inner) {
                 ++step_launches;
-                const StageMaps sm = stage_maps_for(W(cur), Pp(cur), Qq(cur));
-                launch_stage(C, dparams, stage_ptrs(slot), 1, st, &sm, lo, hi - lo);
+                const StagePtrs<T> A = stage_ptrs(slot);
+                const StageMaps sm = stage_maps_for(A);
+                launch_stage(C, dparams, A, 1, st, &sm, lo, hi - lo);
             }
             break;
         }
         case BSQ_PH_STAGE_EDGE: {
             if (!spec_used) {
-                const StageMaps sm = stage_maps_for(W(cur), Pp(cur), Qq(cur));
+                const StagePtrs<T> A = stage_ptrs(slot);
+                const StageMaps sm = stage_maps_for(A);
                 if (stage_inner) {
                     int lo, hi;
                     inner_rows(2, lo, hi);
                     step_launches += (lo > 0) + (hi < d.ny);
-                    launch_stage(C, dparams, stage_ptrs(slot), 1, st, &sm, 0, lo);
-                    launch_stage(C, dparams, stage_ptrs(slot), 1, st, &sm, hi, d.ny - hi);
+                    launch_stage(C, dparams, A, 1, st, &sm, 0, lo);
+                    launch_stage(C, dparams, A, 1, st, &sm, hi, d.ny - hi);
                 } else {
                     ++step_launches;
-                    launch_stage(C, dparams, stage_ptrs(slot), 1, st, &sm);
+                    launch_stage(C, dparams, A, 1, st, &sm);
                 }
                 fold_req = false;
                 ev_mark("stage");
@@ -1167,9 +1193,10 @@ struct Engine : EngineBase {
             frame_restored = false;
             pre("ghost_t");
             ++step_launches;
-            const StageMaps sm = stage_maps_for(W(nxt), Pp(nxt), Qq(nxt));
-            launch_stage(C, pn, stage_ptrs_on(W(nxt), Pp(nxt), Qq(nxt), (slot + 1) % 4, slot, head,
-                                              Wspare()), 1, st, &sm);
+            const StagePtrs<T> A = stage_ptrs_on(W(nxt), Pp(nxt), Qq(nxt), (slot + 1) % 4, slot, head,
+                                                 Wspare());
+            const StageMaps sm = stage_maps_for(A);
+            launch_stage(C, pn, A, 1, st, &sm);
             pre("stage");
             CU(cudaGetLastError());
             spec_pending = true;
@@ -1359,8 +1386,9 @@ struct Engine : EngineBase {
         spec_pending = false;
         CU(cudaMemsetAsync(dres, 0xFF, sizeof(DevResult), st));
         const int slot = (head + 1) % 4;
-        const StageMaps sm = stage_maps_for(W(cur), Pp(cur), Qq(cur));
-        launch_stage(C, dparams, stage_ptrs(slot), 0, st, &sm);
+        const StagePtrs<T> A = stage_ptrs(slot);
+        const StageMaps sm = stage_maps_for(A);
+        launch_stage(C, dparams, A, 0, st, &sm);
         fold_req = false;
         CU(cudaGetLastError());
         int rc;

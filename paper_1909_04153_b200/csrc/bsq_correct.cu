@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) 
             T p_x = (pc[2] - pc[0]) * T(0.5) * C.inv_dx;
             T p_y = (pn[1] - ps[1]) * T(0.5) * C.inv_dy;
             T p_xy = (pn[2] - pn[0] - ps[2] + ps[0]) * T(0.25) * C.inv_dx * C.inv_dy;
-            T sixth = div_static(d[k], C.six, C.r_six);
+            T sixth = div_pos(d[k], C.six, C.r_six);
             T d2 = C.bp13 * d[k] * d[k];
             f = sixth * (dx_[k] * q_y + dy_[k] * q_x) + d2 * q_xy;
             g = sixth * (dx_[k] * p_y + dy_[k] * p_x) + d2 * p_xy;

@@ -32,7 +32,7 @@ constexpr int FX = 32, FY = 8, FR = BSQ_FINAL_FR;  // block 32 x 8 threads, FR r
 constexpr int FG = BSQ_FINAL_FG;  // rows loaded per batch (all loads first, then the work)
 constexpr int FT = FX * FY, FWARPS = FT / 32;
 #ifndef BSQ_FINAL_MINB
-#define BSQ_FINAL_MINB 4
+#define BSQ_FINAL_MINB 3  // 80 registers, no spills (4: 64 with spills, 0.148 vs 0.133 ms)
 #endif
 
 struct Red {
@@ -248,18 +248,25 @@ static __device__ void spec_next(const DevParams &P, double max_rate, DevParams 
 }
 
 
+// Persistent: a grid of (resident CTAs) walks the 32 x 64-cell tiles in a
+// fixed grid-stride order and reduces once at the end (one block reduction,
+// partial and counter per CTA instead of per tile: the per-tile barrier and
+// atomic were the kernel's top stall after the loads).
 template <class T, bool SPIKE, bool FAST>
-__global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, FinalPtrs<T> F) {
+__global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, FinalPtrs<T> F,
+                                                              int tiles_x, int ntiles) {
     __shared__ bool am_last;
     const Layout L = C.L;
     const int nx = L.nx, ny = L.ny;
-    const int I = GL + blockIdx.x * FX + threadIdx.x;
-    const int J0 = GL + blockIdx.y * FR * FY + threadIdx.y;
+    const bool sponges = (C.sponge_len[0] | C.sponge_len[1] | C.sponge_len[2] | C.sponge_len[3]) != 0;
     const long rstep = (long)FY * L.pitch;
+    Acc<T> r{T(0), T(0), T(0), T(0), 0.0, 0};
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int bx = tile % tiles_x, by = tile / tiles_x;
+    const int I = GL + bx * FX + threadIdx.x;
+    const int J0 = GL + by * FR * FY + threadIdx.y;
     const long o0 = L.at(J0, I);
     const bool iin = I < nx + GL;
-    const bool sponges = (C.sponge_len[0] | C.sponge_len[1] | C.sponge_len[2] | C.sponge_len[3]) != 0;
-    Acc<T> r{T(0), T(0), T(0), T(0), 0.0, 0};
 #pragma unroll
     for (int k0 = 0; k0 < FR; k0 += FG) {
         // all loads of the batch first (pure stream), then the work
@@ -334,36 +341,24 @@ __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, Final
             extrema_cell<FAST>(C, w, p, q, be, r);
         }
     }
+    }  // tiles
     Red rr = red_block_warped(red_warp(r));
     const int tid = threadIdx.y * FX + threadIdx.x;
-    // Two-level deterministic fold: the last CTA of each grid row folds that
-    // row's partials (in order) into a row partial; the last row folder folds
-    // the row partials (in order).  Each fold is one round of parallel L2
-    // loads (ld.cg: written by other CTAs before their fence + counter
-    // increment) and a block reduction -- no long serial tail.
-    const int bid = blockIdx.y * gridDim.x + blockIdx.x;
-    Partial *rowp = F.part + (size_t)gridDim.x * gridDim.y;  // one per grid row
+    // Deterministic fold: every CTA writes its partial; the last one to finish
+    // folds them in CTA order (one round of parallel L2 loads -- ld.cg: written
+    // by other CTAs before their fence + counter increment -- and a block
+    // reduction).  The grid-stride tile order is fixed for a given grid, so
+    // the clamped-volume sum is the same every run.
     if (tid == 0) {
-        F.part[bid] = to_partial(rr);
+        F.part[blockIdx.x] = to_partial(rr);
         __threadfence();
-        const unsigned int prev = atomicAdd(&F.counter[1 + blockIdx.y], 1u);
+        const unsigned int prev = atomicAdd(&F.counter[0], 1u);
         am_last = prev == gridDim.x - 1;
     }
     __syncthreads();
     if (!am_last) return;
     __threadfence();
-    const Red row = fold_partials(F.part + (size_t)blockIdx.y * gridDim.x, gridDim.x);
-    if (tid == 0) {
-        rowp[blockIdx.y] = to_partial(row);
-        F.counter[1 + blockIdx.y] = 0u;
-        __threadfence();
-        const unsigned int prev = atomicAdd(&F.counter[0], 1u);
-        am_last = prev == gridDim.y - 1;
-    }
-    __syncthreads();
-    if (!am_last) return;
-    __threadfence();
-    const Red a = fold_partials(rowp, gridDim.y);
+    const Red a = fold_partials(F.part, gridDim.x);
     // gauge cells of the new state (scenario.py:184-202 reads w, P, Q there);
     // other CTAs wrote them: read through L2
     for (int g = tid; g < F.ng; g += FT) {
@@ -443,12 +438,21 @@ int final_rows(int nx, int ny) { return (int)final_grid(nx, ny).y; }
 
 template <class T>
 void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st) {
-    const dim3 grid = final_grid(C.L.nx, C.L.ny), blk(FX, FY);
+    const dim3 tg = final_grid(C.L.nx, C.L.ny), blk(FX, FY);
+    const int ntiles = (int)(tg.x * tg.y);
     const bool fast = flux_fast_rcp_ok(C.h_eps);
-    if (F.spbt)
-        (fast ? k_final<T, true, true> : k_final<T, true, false>)<<<grid, blk, 0, st>>>(C, F);
-    else
-        (fast ? k_final<T, false, true> : k_final<T, false, false>)<<<grid, blk, 0, st>>>(C, F);
+    auto kern = F.spbt ? (fast ? k_final<T, true, true> : k_final<T, true, false>)
+                       : (fast ? k_final<T, false, true> : k_final<T, false, false>);
+    static int resident = 0;  // CTAs of k_final resident on the device (all four share one shape)
+    if (!resident) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, FT, 0);
+        resident = sms * (per > 0 ? per : 1);
+    }
+    const int grid = ntiles < resident ? ntiles : resident;
+    kern<<<grid, blk, 0, st>>>(C, F, (int)tg.x, ntiles);
 }
 
 template <class T>

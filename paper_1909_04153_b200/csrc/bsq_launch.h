@@ -18,6 +18,7 @@ struct StagePtrs {
     T *bu, *bv, *us, *vs;           // quadrature bases and predicted U*, V*
     unsigned long long *bad;        // [5] first non-finite stage cell
     T *maxw;                        // running max of w to fold this state into, or null
+    const T *pf[12];                // phase-D inputs to prefetch: ddx, ddy, h1[0..4], h2[0..4]
 };
 
 template <class T>
@@ -99,6 +100,7 @@ constexpr int STAGE_TX = 32, STAGE_TY = BSQ_STAGE_TY;
 // tile + 2-cell halo, (TX+4) x (TY+4) cells, and of the face beds)
 struct StageMaps {
     CUtensorMap w, p, q, be, dep, bfx, bfy;
+    CUtensorMap pf[12];  // 32 x 8 interior boxes of StagePtrs::pf (L2 prefetch by the TMA unit)
 };
 
 template <class T>

@@ -31,9 +31,18 @@
 
 namespace bsq {
 
+#ifdef BSQ_SOLVE_PARK
+#define SOLVE_WAIT mbar_wait_park
+#else
+#define SOLVE_WAIT mbar_wait
+#endif
+
 constexpr int NLINE = 32;  // lines per CTA
 #ifndef BSQ_SOLVE_NS_ONCHIP
-#define BSQ_SOLVE_NS_ONCHIP 4
+#define BSQ_SOLVE_NS_ONCHIP 3  // stages of SUB chunks (72 KB ring: 2 CTAs per SM)
+#endif
+#ifndef BSQ_SOLVE_SUB
+#define BSQ_SOLVE_SUB 2  // chunks per ring stage (one barrier round trip per SUB chunks)
 #endif
 
 // Ring geometry.  A forward stage holds FT tiles {r, a, den[, rden]}; the
@@ -46,7 +55,9 @@ struct TileGeom {
     static constexpr int FT = ONCHIP ? 3 : 4;                // tiles per forward stage
     static constexpr int NS = ONCHIP ? BSQ_SOLVE_NS_ONCHIP : 6;  // forward ring depth
     static constexpr int NS2 = NS * FT / 2;                  // backward ring depth
-    static constexpr int RING_B = NS * FT * TILE_B;
+    static constexpr int SUB = BSQ_SOLVE_SUB;                // chunks per stage
+    static constexpr int SUBT = SUB * TILE;                  // one operand's slice of a stage
+    static constexpr int RING_B = NS * FT * SUB * TILE_B;
     static constexpr int SMEM_B = 1024 + RING_B + 2 * TILE_B + 8 * (2 * NS + 2 * NS2);
 };
 
@@ -108,25 +119,26 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
     __syncthreads();
 
     // ---- forward sweep --------------------------------------------------------
+    constexpr int SUB = G::SUB, SUBT = G::SUBT;
+    const int nsc = (nc + SUB - 1) / SUB;  // ring stages (super-chunks) per sweep
     if (mode == SOLVE_YBWD) {
         // back substitution only
     } else if (warp == 1) {
         if (lane == 0) {
-            for (int c = 0; c < nc; c++) {
-                const int s = c % NS;
-                if (c >= NS) mbar_wait(&empty[s], ((c / NS) - 1) & 1);
-                int c0, c1;
-                coords(c, c0, c1);
-                T *st = ring + s * FT * TILE;
-                if (RDEN_ONCHIP) {
-                    mbar_expect_tx(&full[s], 3 * G::TILE_B);
-                } else {
-                    mbar_expect_tx(&full[s], 4 * G::TILE_B);
-                    tma_load_2d(st + 3 * TILE, m_rden, c0, c1, &full[s]);
+            for (int u = 0; u < nsc; u++) {
+                const int s = u % NS;
+                if (u >= NS) SOLVE_WAIT(&empty[s], ((u / NS) - 1) & 1);
+                mbar_expect_tx(&full[s], (RDEN_ONCHIP ? 3 : 4) * SUB * G::TILE_B);
+#pragma unroll
+                for (int j = 0; j < SUB; j++) {
+                    int c0, c1;
+                    coords(u * SUB + j, c0, c1);
+                    T *st = ring + s * FT * SUBT + j * TILE;
+                    if (!RDEN_ONCHIP) tma_load_2d(st + 3 * SUBT, m_rden, c0, c1, &full[s]);
+                    tma_load_2d(st, m_rhs, c0, c1, &full[s]);
+                    tma_load_2d(st + SUBT, m_a, c0, c1, &full[s]);
+                    tma_load_2d(st + 2 * SUBT, m_den, c0, c1, &full[s]);
                 }
-                tma_load_2d(st, m_rhs, c0, c1, &full[s]);
-                tma_load_2d(st + TILE, m_a, c0, c1, &full[s]);
-                tma_load_2d(st + 2 * TILE, m_den, c0, c1, &full[s]);
             }
         }
     } else {
@@ -150,16 +162,16 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
             return POS ? div_static_pos(num, den, nr) : div_static(num, den, -nr);
         };
         auto nrden = [&](const T *st, int t) -> T {
-            return RDEN_ONCHIP ? -rcp_rn_inrange(st[2 * TILE + t]) : st[3 * TILE + t];
+            return RDEN_ONCHIP ? -rcp_rn_inrange(st[2 * SUBT + t]) : st[3 * SUBT + t];
         };
         T dw = T(0);
         for (int c = 0; c < nc; c++) {
-            const int s = c % NS;
-            T *st = ring + s * FT * TILE;
+            const int u = c / SUB, j = c % SUB, s = u % NS;
+            T *st = ring + s * FT * SUBT + j * TILE;
             T *ob = outb + (c & 1) * TILE;
             if (lane == 0) bulk_wait_read<1>();  // the store from this out tile (c-2) has read it
             __syncwarp();
-            mbar_wait(&full[s], (c / NS) & 1);
+            if (j == 0) SOLVE_WAIT(&full[s], (u / NS) & 1);
             const int kmax = min(EK, n - c * EK);
             // the whole chunk goes to registers first: the ring and the out tile
             // share one smem base, so interleaved loads could not be hoisted past
@@ -170,9 +182,9 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                 for (int k = 0; k < EK; k++) {
                     const int t = toff<T, XDIR>(lane, k);
                     rv[k] = st[t];
-                    av[k] = st[TILE + t];
-                    dv[k] = st[2 * TILE + t];
-                    nv[k] = RDEN_ONCHIP ? T(0) : st[3 * TILE + t];
+                    av[k] = st[SUBT + t];
+                    dv[k] = st[2 * SUBT + t];
+                    nv[k] = RDEN_ONCHIP ? T(0) : st[3 * SUBT + t];
                 }
                 if (RDEN_ONCHIP) {
 #pragma unroll
@@ -190,12 +202,12 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                     const int t = toff<T, XDIR>(lane, k);
                     const int e = c * EK + k;
                     T r = st[t];
-                    const T a = st[TILE + t];
+                    const T a = st[SUBT + t];
                     if (e == 0) {  // folded, no recurrence term (thomas_batch dw[0])
-                        dw = step(r - a * g0, st[2 * TILE + t], nrden(st, t));
+                        dw = step(r - a * g0, st[2 * SUBT + t], nrden(st, t));
                     } else {
                         if (e == n - 1) r = r - cl * g1;  // far ghost
-                        dw = step(r - a * dw, st[2 * TILE + t], nrden(st, t));
+                        dw = step(r - a * dw, st[2 * SUBT + t], nrden(st, t));
                     }
                     ob[t] = dw;
                 }
@@ -203,7 +215,7 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&empty[s]);
+                if (j == SUB - 1 || c == nc - 1) mbar_arrive(&empty[s]);
                 int c0, c1;
                 coords(c, c0, c1);
                 tma_store_2d(m_out, c0, c1, ob);
@@ -223,15 +235,18 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
         // forward sweep only
     } else if (warp == 1) {
         if (lane == 0) {
-            for (int s_ = 0; s_ < nc; s_++) {
-                const int c = nc - 1 - s_, s = s_ % NS2;
-                if (s_ >= NS2) mbar_wait(&empty2[s], ((s_ / NS2) - 1) & 1);
-                mbar_expect_tx(&full2[s], 2 * G::TILE_B);
-                int c0, c1;
-                coords(c, c0, c1);
-                T *st = ring + s * 2 * TILE;
-                tma_load_2d(st, m_out, c0, c1, &full2[s]);
-                tma_load_2d(st + TILE, m_cw, c0, c1, &full2[s]);
+            for (int v = 0; v < nsc; v++) {  // super-chunks from the line's end
+                const int u = nsc - 1 - v, s = v % NS2;
+                if (v >= NS2) SOLVE_WAIT(&empty2[s], ((v / NS2) - 1) & 1);
+                mbar_expect_tx(&full2[s], 2 * SUB * G::TILE_B);
+#pragma unroll
+                for (int j = 0; j < SUB; j++) {
+                    int c0, c1;
+                    coords(u * SUB + j, c0, c1);
+                    T *st = ring + s * 2 * SUBT + j * TILE;
+                    tma_load_2d(st, m_out, c0, c1, &full2[s]);
+                    tma_load_2d(st + SUBT, m_cw, c0, c1, &full2[s]);
+                }
             }
         }
     } else {
@@ -241,12 +256,12 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
         const T xn = (nint && lv) ? S.x_in[line] : T(0);
         T xv = T(0);
         for (int s_ = 0; s_ < nc; s_++) {
-            const int c = nc - 1 - s_, s = s_ % NS2;
-            T *st = ring + s * 2 * TILE;
+            const int c = nc - 1 - s_, u = c / SUB, j = c % SUB, v = nsc - 1 - u, s = v % NS2;
+            T *st = ring + s * 2 * SUBT + j * TILE;
             T *ob = outb + (s_ & 1) * TILE;
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
-            mbar_wait(&full2[s], (s_ / NS2) & 1);
+            if (c == min(u * SUB + SUB - 1, nc - 1)) SOLVE_WAIT(&full2[s], (v / NS2) & 1);
             const int kmax = min(EK, n - c * EK);
             if (s_ > 0 && kmax == EK) {  // interior chunk
                 T dv[EK], cv[EK];
@@ -254,7 +269,7 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                 for (int k = 0; k < EK; k++) {
                     const int t = toff<T, XDIR>(lane, k);
                     dv[k] = st[t];
-                    cv[k] = st[TILE + t];
+                    cv[k] = st[SUBT + t];
                 }
 #pragma unroll
                 for (int k = EK - 1; k >= 0; k--) {
@@ -267,16 +282,16 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                 for (int k = kmax - 1; k >= 0; k--) {
                     const int t = toff<T, XDIR>(lane, k);
                     if (s_ == 0 && k == kmax - 1)
-                        xv = nint ? st[t] - st[TILE + t] * xn : st[t];
+                        xv = nint ? st[t] - st[SUBT + t] * xn : st[t];
                     else
-                        xv = st[t] - st[TILE + t] * xv;
+                        xv = st[t] - st[SUBT + t] * xv;
                     ob[t] = xv;
                 }
             }
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&empty2[s]);
+                if (j == 0) mbar_arrive(&empty2[s]);
                 int c0, c1;
                 coords(c, c0, c1);
                 tma_store_2d(m_out, c0, c1, ob);

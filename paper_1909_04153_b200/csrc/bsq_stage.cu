@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
 
     const int I = I0 + lane, x = lane + 2;  // this lane's column (padded / smem)
     const int jw = J0 + warp * SR;          // first row of this warp
-    const T g = C.g, h_eps = C.h_eps, theta = C.theta;
+    const T g = C.g, hg = C.half_g, h_eps = C.h_eps, theta = C.theta;
     // bed on face (J, col) -- clamped to the array for out-of-grid lanes
     auto bfx_at = [&](int J, int col) -> T {
         return (J < nyt && col <= nx + 2) ? A.bfx[L.at(J, col)] : T(0);
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
         const T b31 = bfx_at(J, I0 + 31);
         const Faces<T> fl = xfaces(yy, SW_ + 1, b31, bfx_at(J, I0 + 30));
         const Faces<T> fr = xfaces(yy, SW_ + 2, bfx_at(J, I0 + 32), b31);
-        cu_flux_rcp(fl.whi, fr.wlo, fl.phi, fr.plo, fl.qhi, fr.qlo, b31, g, h_eps, fe1, fe2, fe3);
+        cu_flux_rcp(fl.whi, fr.wlo, fl.phi, fr.plo, fl.qhi, fr.qlo, b31, g, hg, h_eps, fe1, fe2, fe3);
     }
 
     // ---- y pre-pass: faces of rows jw-1 and jw, flux through their face ---------
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
         const Faces<T> ys = yfaces(yy - 1, x, bfy_s, bfy_at(jw - 2, I));
         yc = yfaces(yy, x, bfy_n, bfy_s);
         T fq, fp;  // normal momentum is Q, tangential is P: fy2 = P flux, fy3 = Q flux
-        cu_flux_rcp(ys.whi, yc.wlo, ys.qhi, yc.qlo, ys.phi, yc.plo, bfy_s, g, h_eps, fs1, fq, fp);
+        cu_flux_rcp(ys.whi, yc.wlo, ys.qhi, yc.qlo, ys.phi, yc.plo, bfy_s, g, hg, h_eps, fs1, fq, fp);
         fs2 = fp;
         fs3 = fq;
     }
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
             lq = eq;
         }
         T fw1, fw2, fw3;  // flux through the west face of this cell
-        cu_flux_rcp(lw, xf.wlo, lp, xf.plo, lq, xf.qlo, bx_w, g, h_eps, fw1, fw2, fw3);
+        cu_flux_rcp(lw, xf.wlo, lp, xf.plo, lq, xf.qlo, bx_w, g, hg, h_eps, fw1, fw2, fw3);
         T fe_1 = shfl_dn1(fw1), fe_2 = shfl_dn1(fw2), fe_3 = shfl_dn1(fw3);
         const T g1 = shfl_idx(fe1, r), g2 = shfl_idx(fe2, r), g3 = shfl_idx(fe3, r);
         if (lane == SW_ - 1) {
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
         // -- y: faces of row J+1, flux through the J|J+1 face (carried north) --
         const Faces<T> yn = yfaces(yy + 1, x, bfy_nn, bfy_n);
         T fn1, fnq, fnp;
-        cu_flux_rcp(yc.whi, yn.wlo, yc.qhi, yn.qlo, yc.phi, yn.plo, bfy_n, g, h_eps, fn1, fnq, fnp);
+        cu_flux_rcp(yc.whi, yn.wlo, yc.qhi, yn.qlo, yc.phi, yn.plo, bfy_n, g, hg, h_eps, fn1, fnq, fnp);
         const T fn2 = fnp, fn3 = fnq;
 
         cp_async_wait_all();  // this lane's cell inputs have landed
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
                 const T p_y = (Pp[yy + 1][x] - Pp[yy - 1][x]) * T(0.5) * C.inv_dy;
                 const T p_xy = (Pp[yy + 1][x + 1] - Pp[yy + 1][x - 1] - Pp[yy - 1][x + 1] +
                                 Pp[yy - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
-                const T sixth = div_static(d, C.six, C.r_six);
+                const T sixth = div_pos(d, C.six, C.r_six);
                 const T d2 = C.bp13 * d * d;
                 fs_ = sixth * (dx_ * q_y + dy_ * q_x) + d2 * q_xy;
                 gs_ = sixth * (dx_ * p_y + dy_ * p_x) + d2 * p_xy;
@@ -300,14 +300,14 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
                 // U*, V* (dispersion.py:131-148): divisions by grid constants
                 const T pe = S.p[yy][x + 1], pw = S.p[yy][x - 1];
                 const T qn = S.q[yy + 1][x], qs = S.q[yy - 1][x];
-                const T p_x = div_static(pe - pw, C.two_dx, C.r_two_dx);
-                const T p_xx = div_static(pe - T(2) * pc + pw, C.dx2, C.r_dx2);
+                const T p_x = div_pos(pe - pw, C.two_dx, C.r_two_dx);
+                const T p_xx = div_pos(pe - T(2) * pc + pw, C.dx2, C.r_dx2);
                 const T ustar =
-                    pc - div_static(d * dx_, C.three, C.r_three) * p_x - C.bp13 * d * d * p_xx;
-                const T q_y = div_static(qn - qs, C.two_dy, C.r_two_dy);
-                const T q_yy = div_static(qn - T(2) * qc + qs, C.dy2, C.r_dy2);
+                    pc - div_pos(d * dx_, C.three, C.r_three) * p_x - C.bp13 * d * d * p_xx;
+                const T q_y = div_pos(qn - qs, C.two_dy, C.r_two_dy);
+                const T q_yy = div_pos(qn - T(2) * qc + qs, C.dy2, C.r_dy2);
                 const T vstar =
-                    qc - div_static(d * dy_, C.three, C.r_three) * q_y - C.bp13 * d * d * q_yy;
+                    qc - div_pos(d * dy_, C.three, C.r_three) * q_y - C.bp13 * d * d * q_yy;
                 // predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
                 T wn, bu, bv, us, vs;
                 if (P->euler) {

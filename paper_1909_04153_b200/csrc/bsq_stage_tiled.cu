@@ -71,7 +71,7 @@ struct StageSmem {
 
 template <class T, bool FR>
 __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const DevParams *__restrict__ P,
-                                                 StagePtrs<T> A, int predict,
+                                                 const __grid_constant__ StagePtrs<T> A, int predict,
                                                  const __grid_constant__ StageMaps M, int row0) {
     // the TMA destinations need 128-B alignment: the kernel has no static
     // smem, so the dynamic window starts at the CTA's smem base (checked)
@@ -107,6 +107,12 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     }
     // phase D's per-cell inputs that phase A does not read: start them towards
     // L2 now (no registers held), so phase D's loads hit on chip
+#ifndef BSQ_STAGE_LANE_PREFETCH
+    if (tid == 0) {  // the TMA unit fetches the 32 x 8 boxes
+        const int na = (predict && !P->euler) ? 12 : 2;
+        for (int k = 0; k < na; k++) tma_prefetch_2d(&M.pf[k], L.xo + I0 - GL + 2, J0);
+    }
+#else
     {
         // lane k < 24 of warp ty: array k >> 1 (ddx, ddy, h1[0..4], h2[0..4]),
         // 128-B line k & 1 of the warp's 256-B tile row
@@ -115,11 +121,15 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         const int na = (predict && !P->euler) ? 12 : 2;
         if (tx < 2 * na && Jc < ny + GL && Ic < nx + GL) {
             const int k = tx >> 1;
-            const T *base = k == 0 ? A.ddx : k == 1 ? A.ddy : k < 7 ? A.h1[k - 2] : A.h2[k - 7];
-            prefetch_l2(base + L.at(Jc, Ic));
+            prefetch_l2(A.pf[k] + L.at(Jc, Ic));  // one indexed constant load
         }
     }
+#endif
+#ifdef BSQ_STAGE_SPIN
     mbar_wait(&S.bar, 0);
+#else
+    mbar_wait_park(&S.bar, 0);
+#endif
     // ---- B: faces, once per cell, + eta -----------------------------------------
     // Warp ty, lane tx (2-D map: no div/mod, no warp covering two kinds):
     //   round 0  x faces of tile row ty, face columns 0..31
@@ -176,7 +186,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         T f1, f2, f3;
         cu_flux_rcp<FR>(S.f.xhi[0][r][xi], S.f.xlo[0][r][xi + 1], S.f.xhi[1][r][xi],
                     S.f.xlo[1][r][xi + 1], S.f.xhi[2][r][xi], S.f.xlo[2][r][xi + 1],
-                    S.bfx[r][xi + 1], C.g, C.h_eps, f1, f2, f3);
+                    S.bfx[r][xi + 1], C.g, C.half_g, C.h_eps, f1, f2, f3);
         S.f.xhi[0][r][xi] = f1;
         S.f.xhi[1][r][xi] = f2;
         S.f.xhi[2][r][xi] = f3;
@@ -185,7 +195,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         T f1, fq, fp;
         cu_flux_rcp<FR>(S.f.yhi[0][yi][c], S.f.ylo[0][yi + 1][c], S.f.yhi[2][yi][c],
                     S.f.ylo[2][yi + 1][c], S.f.yhi[1][yi][c], S.f.ylo[1][yi + 1][c],
-                    S.bfy[yi + 1][c], C.g, C.h_eps, f1, fq, fp);
+                    S.bfy[yi + 1][c], C.g, C.half_g, C.h_eps, f1, fq, fp);
         S.f.yhi[0][yi][c] = f1;
         S.f.yhi[1][yi][c] = fp;  // fy2 carries P
         S.f.yhi[2][yi][c] = fq;  // fy3 carries Q
@@ -261,7 +271,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         const T p_y = (S.p[y + 1][x] - S.p[y - 1][x]) * T(0.5) * C.inv_dy;
         const T p_xy = (S.p[y + 1][x + 1] - S.p[y + 1][x - 1] - S.p[y - 1][x + 1] +
                         S.p[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
-        const T sixth = div_static(d, C.six, C.r_six);
+        const T sixth = div_pos(d, C.six, C.r_six);
         const T d2 = C.bp13 * d * d;
         fs_ = sixth * (dx_ * q_y + dy_ * q_x) + d2 * q_xy;
         gs_ = sixth * (dx_ * p_y + dy_ * p_x) + d2 * p_xy;
@@ -288,12 +298,12 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     if (!predict) return;
 
     // U*, V* (dispersion.py:131-148): divisions by grid constants
-    const T p_x = div_static(S.p[y][x + 1] - S.p[y][x - 1], C.two_dx, C.r_two_dx);
-    const T p_xx = div_static(S.p[y][x + 1] - T(2) * pc + S.p[y][x - 1], C.dx2, C.r_dx2);
-    const T ustar = pc - div_static(d * dx_, C.three, C.r_three) * p_x - C.bp13 * d * d * p_xx;
-    const T q_y = div_static(S.q[y + 1][x] - S.q[y - 1][x], C.two_dy, C.r_two_dy);
-    const T q_yy = div_static(S.q[y + 1][x] - T(2) * qc + S.q[y - 1][x], C.dy2, C.r_dy2);
-    const T vstar = qc - div_static(d * dy_, C.three, C.r_three) * q_y - C.bp13 * d * d * q_yy;
+    const T p_x = div_pos(S.p[y][x + 1] - S.p[y][x - 1], C.two_dx, C.r_two_dx);
+    const T p_xx = div_pos(S.p[y][x + 1] - T(2) * pc + S.p[y][x - 1], C.dx2, C.r_dx2);
+    const T ustar = pc - div_pos(d * dx_, C.three, C.r_three) * p_x - C.bp13 * d * d * p_xx;
+    const T q_y = div_pos(S.q[y + 1][x] - S.q[y - 1][x], C.two_dy, C.r_two_dy);
+    const T q_yy = div_pos(S.q[y + 1][x] - T(2) * qc + S.q[y - 1][x], C.dy2, C.r_dy2);
+    const T vstar = qc - div_pos(d * dy_, C.three, C.r_three) * q_y - C.bp13 * d * d * q_yy;
 
     // predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
     T wn, bu, bv, us, vs;
@@ -332,8 +342,15 @@ static void launch_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs
                              (int)smem);
         attr_set = true;
     }
+    StagePtrs<T> Ap = A;
+    Ap.pf[0] = A.ddx;
+    Ap.pf[1] = A.ddy;
+    for (int k = 0; k < 5; k++) {
+        Ap.pf[2 + k] = A.h1[k];
+        Ap.pf[7 + k] = A.h2[k];
+    }
     dim3 grid((C.L.nx + tiled::TX - 1) / tiled::TX, (nrows + tiled::TY - 1) / tiled::TY);
-    tiled::k_stage<T, FR><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, A, predict, *M,
+    tiled::k_stage<T, FR><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, Ap, predict, *M,
                                                                          row0);
 }
 
