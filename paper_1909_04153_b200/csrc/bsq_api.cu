@@ -9,6 +9,7 @@
 // contraction disabled (-ffp-contract=off), so it reproduces the reference's
 // numpy/numba values bit for bit (implicit.py:84-119, _kernels.py:360-378).
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <limits>
@@ -22,6 +23,16 @@
 #include "bsq_launch.h"
 
 using namespace bsq;
+
+bool bsq::pdl_on() {
+    static const int on = [] {
+        // off by default: measured 1.848 -> 1.860 ms per step with it on (the
+        // early-resident CTAs of the next kernel take slots from the tail)
+        const char *e = std::getenv("BSQ_PDL");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return on != 0;
+}
 
 static thread_local std::string g_err;
 

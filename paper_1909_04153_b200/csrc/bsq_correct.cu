@@ -26,6 +26,8 @@ __host__ __device__ constexpr int cr_rows() { return sizeof(T) == 8 ? BSQ_CORREC
 template <class T>
 __global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) {
     constexpr int CR = cr_rows<T>();
+    pdl_trigger();
+    pdl_wait();
     const Layout L = C.L;
     const int I = GL + blockIdx.x * 32 + threadIdx.x;
     const int J0 = GL + (blockIdx.y * 8 + threadIdx.y) * CR;
@@ -101,7 +103,7 @@ void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st
         Cb.L.ny = nrows;
     }
     dim3 grid((C.L.nx + 31) / 32, (nrows + 8 * CR - 1) / (8 * CR));  // 32 x (8*CR) cells
-    k_correct<T><<<grid, dim3(32, 8), 0, st>>>(Cb, Kb);
+    launch_k(k_correct<T>, grid, dim3(32, 8), 0, st, Cb, Kb);
 }
 
 #if BSQ_INST_F64

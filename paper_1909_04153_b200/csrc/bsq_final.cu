@@ -256,6 +256,8 @@ template <class T, bool SPIKE, bool FAST>
 __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, FinalPtrs<T> F,
                                                               int tiles_x, int ntiles) {
     __shared__ bool am_last;
+    pdl_trigger();
+    pdl_wait();
     const Layout L = C.L;
     const int nx = L.nx, ny = L.ny;
     const bool sponges = (C.sponge_len[0] | C.sponge_len[1] | C.sponge_len[2] | C.sponge_len[3]) != 0;
@@ -452,7 +454,7 @@ void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st) {
         resident = sms * (per > 0 ? per : 1);
     }
     const int grid = ntiles < resident ? ntiles : resident;
-    kern<<<grid, blk, 0, st>>>(C, F, (int)tg.x, ntiles);
+    launch_k(kern, dim3(grid), blk, 0, st, C, F, (int)tg.x, ntiles);
 }
 
 template <class T>

@@ -57,6 +57,8 @@ __device__ __forceinline__ long frame_index(int nx, int ny, int J, int I) {
 template <class T>
 __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which, const T *src_w,
                         const T *src_p, const T *src_q, T *dst_w, T *dst_p, T *dst_q, T *save) {
+    pdl_trigger();
+    pdl_wait();
     const int nx = C.L.nx, ny = C.L.ny, nxt = nx + 4, nyt = ny + 4;
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     const T *src[3] = {src_w, src_p, src_q};
@@ -162,7 +164,8 @@ template <class T>
 void launch_ghost(const Consts<T> &C, const DevParams *P, int which, const T *sw, const T *sp,
                   const T *sq, T *dw, T *dp, T *dq, cudaStream_t st, T *save) {
     int n = 4 * (C.L.ny + 4) + 4 * C.L.nx;
-    k_ghost<T><<<(n + 127) / 128, 128, 0, st>>>(C, P, which, sw, sp, sq, dw, dp, dq, save);
+    launch_k(k_ghost<T>, dim3((n + 127) / 128), dim3(128), 0, st, C, P, which, sw, sp, sq, dw, dp, dq,
+             save);
 }
 
 #if BSQ_INST_F64

@@ -7,6 +7,29 @@
 
 namespace bsq {
 
+// whether the step's kernels are launched as programmatic dependents of
+// their predecessors (BSQ_PDL=1; off by default, bsq_api.cu)
+bool pdl_on();
+
+// <<<g, b, smem, st>>> with the programmatic-stream-serialization attribute
+// when pdl_on(): the kernel must call pdl_wait() before reading what earlier
+// work on the stream wrote
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st,
+                     Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 template <class T>
 struct StagePtrs {
     const T *w, *p, *q;             // committed state, ghost-filled at t

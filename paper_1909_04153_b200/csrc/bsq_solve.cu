@@ -310,6 +310,8 @@ __global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_cons
     extern __shared__ unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    pdl_trigger();
+    pdl_wait();
     if ((int)blockIdx.x < nbx)
         solve_lines_tma<T, true, POS, ONCHIP>(C, M, S, blockIdx.x * NLINE, smem, mode);
     else
@@ -341,13 +343,13 @@ void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
 #endif
     dim3 g(bx + nby), b(64);
     if (pos && onchip)
-        k_solve_tma<T, true, true><<<g, b, smem_on, st>>>(C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, true, true>, g, b, smem_on, st, C, M, S, bx, mode);
     else if (pos)
-        k_solve_tma<T, true, false><<<g, b, smem_off, st>>>(C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, true, false>, g, b, smem_off, st, C, M, S, bx, mode);
     else if (onchip)
-        k_solve_tma<T, false, true><<<g, b, smem_on, st>>>(C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, false, true>, g, b, smem_on, st, C, M, S, bx, mode);
     else
-        k_solve_tma<T, false, false><<<g, b, smem_off, st>>>(C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, false, false>, g, b, smem_off, st, C, M, S, bx, mode);
 }
 
 #if BSQ_INST_F64

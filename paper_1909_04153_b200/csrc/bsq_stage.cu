@@ -80,6 +80,8 @@ __global__ void __launch_bounds__(SW_ *SNW, 4) k_stage(Consts<T> C, const DevPar
                                                    StagePtrs<T> A, int predict, int row0) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StageSmem<T> &S = *reinterpret_cast<StageSmem<T> *>(smem_raw);
+    pdl_trigger();
+    pdl_wait();
     const Layout L = C.L;
     const int nx = L.nx, ny = L.ny, nxt = nx + 4, nyt = ny + 4;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -370,7 +372,7 @@ void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A,
             attr_set = true;
         }
         dim3 grid((C.L.nx + SW_ - 1) / SW_, (nrows + STY - 1) / STY);
-        k_stage<T><<<grid, SW_ * SNW, smem, st>>>(C, P, A, predict, row0);
+        launch_k(k_stage<T>, grid, dim3(SW_ * SNW), smem, st, C, P, A, predict, row0);
     }
 }
 

@@ -78,6 +78,8 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     extern __shared__ __align__(128) unsigned char smem_raw[];
     StageSmem<T> &S = *reinterpret_cast<StageSmem<T> *>(smem_raw);
     if (threadIdx.x == 0 && threadIdx.y == 0 && (smem_u32(smem_raw) & 127u) != 0) __trap();
+    pdl_trigger();
+    pdl_wait();
     const Layout L = C.L;
     const int nx = L.nx, ny = L.ny;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
@@ -350,8 +352,8 @@ static void launch_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs
         Ap.pf[7 + k] = A.h2[k];
     }
     dim3 grid((C.L.nx + tiled::TX - 1) / tiled::TX, (nrows + tiled::TY - 1) / tiled::TY);
-    tiled::k_stage<T, FR><<<grid, dim3(tiled::TX, tiled::TY), smem, st>>>(C, P, Ap, predict, *M,
-                                                                         row0);
+    launch_k(tiled::k_stage<T, FR>, grid, dim3(tiled::TX, tiled::TY), smem, st, C, P, Ap, predict,
+             *M, row0);
 }
 
 template <class T>

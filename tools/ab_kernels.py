@@ -34,6 +34,17 @@ sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
 sim.speculate = not a.no_spec
 for _ in range(4):
     sim.advance()
+# whole-step device time without per-kernel events (they would split the
+# launches PDL lets overlap)
+st = sim._dev.stream
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize()
+ev0.record(st)
+for _ in range(a.steps):
+    sim.advance()
+ev1.record(st)
+torch.cuda.synchronize()
+step_dev = ev0.elapsed_time(ev1) / a.steps
 sim._dev.set_timing(True)
 acc, n = {}, 0
 torch.cuda.synchronize()
@@ -46,5 +57,5 @@ for _ in range(a.steps):
 torch.cuda.synchronize()
 wall = (time.perf_counter() - t0) / n * 1e3
 print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "spec": not a.no_spec,
-                  "step_ms_wall": round(wall, 4),
+                  "step_ms_dev": round(step_dev, 4), "step_ms_wall": round(wall, 4),
                   **{k: round(v / n, 4) for k, v in acc.items()}}))
