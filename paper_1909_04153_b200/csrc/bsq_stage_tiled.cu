@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         }
     }
 #endif
-#ifdef BSQ_STAGE_SPIN
+#if defined(BSQ_STAGE_SPIN)
     mbar_wait(&S.bar, 0);
 #else
     mbar_wait_park(&S.bar, 0);
