@@ -185,6 +185,67 @@ def cpu_baseline(case, steps: int, threads: int):
     return cells * steps / dt / 1e9, dt
 
 
+# BASELINE configs measured beside the headline: (device steps timed, warm-up,
+# CPU-oracle sample steps, the reference's single-core numba ms/step from
+# BASELINE.md section 2)
+SIDE_CONFIGS = {
+    "C1": dict(steps=400, warmup=5, cpu_steps=200, numba_ms=2.40,
+               what="solitary wave, 1024x5 (BASELINE configs[0]; 1024x5 interior as SURVEY App. D)"),
+    "C2": dict(steps=400, warmup=5, cpu_steps=20, numba_ms=59.8,
+               what="plane-beach runup, 2048x64, h_dry=1e-3 (configs[1])"),
+    "C3": dict(steps=100, warmup=5, cpu_steps=3, numba_ms=522.0,
+               what="elliptic shoal, 1024x1024, sine maker + sponges (configs[2])"),
+}
+
+
+def config_line(name, dev, hbm, no_cpu=False):
+    """Device ms/step and Gcell/s of one BASELINE config (fp64, adaptive,
+    bitwise = reference), its HBM step fraction at B_alg, and the CPU oracle
+    on a bounded sample of the same run."""
+    import torch
+    from paper_1909_04153_b200 import stepper
+    from paper_1909_04153_b200.scenario import make_case
+    spec = SIDE_CONFIGS[name]
+    case = make_case(name)
+    cells = case.bathy.grid.nx * case.bathy.grid.ny
+    sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
+                            stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
+                            h_dry=case.h_dry, device=dev)
+    for _ in range(spec["warmup"]):
+        sim.advance()
+    st = sim._dev.stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(st)
+    for _ in range(spec["steps"]):
+        sim.advance()
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / spec["steps"]
+    sim.close()
+    gcs = cells / (ms * 1e-3) / 1e9
+    out = {"workload": spec["what"], "cells": cells, "steps": spec["steps"],
+           "warmup": spec["warmup"], "ms_per_step": ms, "value": gcs, "unit": "Gcell-updates/s",
+           "step_frac": gcs * B_ALG_STEP / hbm,
+           "reference_numba_1core_ms_per_step": spec["numba_ms"],
+           "speedup_vs_numba_1core": spec["numba_ms"] / ms}
+    if not no_cpu:
+        threads = cpu_threads()
+        v, wall = cpu_baseline(case, spec["cpu_steps"], threads)
+        out["cpu_baseline"] = {"value": v, "unit": "Gcell-updates/s", "cores": threads,
+                               "kind": "port", "ms_per_step": wall / spec["cpu_steps"] * 1e3,
+                               "sample": f"{spec['cpu_steps']} steps after 1 warm-up"}
+    return out
+
+
+def cpu_threads() -> int:
+    """Host threads the CPU legs use: the logical CPUs this process may run on."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def config_dict(args, case, world, g=None):
     g = g or case.bathy.grid
     return {"workload": f"C5 rip channel + JONSWAP maker, 4096x4096 per GPU, global "
@@ -218,7 +279,7 @@ def _run_reference(args):
     from oracle import oracle as orc
     from paper_1909_04153_b200.scenario import make_case
     case = make_case("C4", scale=args.scale)
-    threads = os.cpu_count() or 1
+    threads = cpu_threads()
     sim = orc.OracleSimulator(case.bathy, case.state.copy(), case.boundaries,
                               orc.OController(dt_init=case.dt_init), phys=case.phys,
                               h_dry=case.h_dry, threads=threads)
@@ -255,6 +316,7 @@ def main():
     ap.add_argument("--scale", type=int, default=1, help="divide the grid (debug only)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-steps", type=int, default=6)  # ~10 s of oracle work at 4096^2
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1/C2/C3 side fields")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -395,6 +457,7 @@ def main():
                 "traffic_source": tr.get("source") if tk else None,
                 "peak_kind": peak_kind,
                 "kernel_ms": avg, "step_achieved": step_gbs, "step_frac": step_gbs / hbm,
+                "step_frac_nominal_8tbs": step_gbs / 8000.0,
                 "step_bytes_per_cell": B_ALG_STEP}
 
     # ---- e2e through the public API from pinned host buffers --------------------
@@ -427,10 +490,15 @@ def main():
                        "(static upload + LU factorization)"}
     sim.close()
 
+    # ---- the other BASELINE configurations (rank 0, N = 1; side fields) --------------
+    configs = None
+    if rank == 0 and world == 1 and args.scale == 1 and not args.no_configs:
+        configs = {k: config_line(k, dev, hbm, args.no_cpu) for k in ("C1", "C2", "C3")}
+
     # ---- CPU baseline (rank 0, N = 1 only) ------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
+        threads = cpu_threads()
         v_cpu, wall = cpu_baseline(case, args.cpu_steps, threads)
         cpu = {"value": v_cpu, "unit": "Gcell-updates/s", "cores": threads, "kind": "port",
                "sample": f"{args.cpu_steps} full {case.bathy.grid.nx}x{case.bathy.grid.ny} steps "
@@ -444,6 +512,7 @@ def main():
             "data": "synthetic (rip-channel bathymetry, JONSWAP maker; reference generators)",
             "config": config_dict(args, case, world, gg), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": kps * args.steps, "clocks": clock_info, "fp32": fp32,
+            "configs": configs,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

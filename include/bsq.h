@@ -280,6 +280,12 @@ int bsq_kernel_times(bsq_ctx *ctx, int max_n, float *ms, const char **names, int
  * includes the next step's queued ghost + stage, and excludes its own) */
 int bsq_kernels_per_step(bsq_ctx *ctx);
 
+/* -- test seam: the device quotient helpers on host arrays ----------------
+ * out[i] = x[i] / d[i] as computed by helper `op` (bsq_check.cu): 0
+ * div_static, 1 div_pos, 2 div_rcp, 3 div_rcp_pos, 4 div_nonneg, 5
+ * div_static_pos, 6 the hardware IEEE division.  fp64. */
+int bsq_check_quotients(int op, const double *x, const double *d, long n, double *out);
+
 #ifdef __cplusplus
 }
 #endif

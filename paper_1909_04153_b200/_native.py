@@ -117,6 +117,7 @@ SIGNATURES = [
     ("bsq_max_tracker", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     ("bsq_download_max", ctypes.c_int, [ctypes.c_void_p, _dp]),
     ("bsq_maker_sums", ctypes.c_int, [_dp, ctypes.c_int, ctypes.c_double, _dp]),
+    ("bsq_check_quotients", ctypes.c_int, [ctypes.c_int, _dp, _dp, ctypes.c_long, _dp]),
     ("bsq_append_rows", ctypes.c_longlong, [ctypes.c_char_p, _dp, ctypes.c_long, ctypes.c_long,
                                             ctypes.c_long, ctypes.c_int]),
 ]

@@ -28,7 +28,7 @@ SRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(OUT_DIR, "libbsq.so")
 KERNEL_SOURCES = ["bsq_ghost.cu", "bsq_stage.cu", "bsq_stage_tiled.cu", "bsq_solve.cu", "bsq_cr.cu",
-                  "bsq_spike.cu", "bsq_correct.cu", "bsq_final.cu"]
+                  "bsq_spike.cu", "bsq_correct.cu", "bsq_final.cu", "bsq_check.cu"]
 HOST_SOURCES = ["bsq_api.cu", "bsq_io.cpp"]
 SOURCES = KERNEL_SOURCES + HOST_SOURCES
 # fp32 objects keep --fmad=false where the file also runs fp64 scalar code that

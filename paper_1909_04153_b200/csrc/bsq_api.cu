@@ -1676,6 +1676,12 @@ int bsq_kernel_times(bsq_ctx *c, int max_n, float *ms, const char **names, int *
     })());
 }
 
+int bsq_check_quotients(int op, const double *x, const double *d, long n, double *out) {
+    if (!x || !d || !out || n < 0 || op < 0 || op > 6) return fail(BSQ_ERR_BAD_ARG, "bad arguments");
+    if (n == 0) return BSQ_OK;
+    return check_quotients(op, x, d, n, out) ? fail(BSQ_ERR_CUDA, "quotient check failed") : BSQ_OK;
+}
+
 int bsq_kernels_per_step(bsq_ctx *c) {
     if (!c) return 0;
     return ENGINE(c, (int)(e->step_launches ? e->step_launches : (e->d.cross_correction ? 7 : 5)));

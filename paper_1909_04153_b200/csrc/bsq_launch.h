@@ -10,6 +10,8 @@ namespace bsq {
 // whether the step's kernels are launched as programmatic dependents of
 // their predecessors (BSQ_PDL=1; off by default, bsq_api.cu)
 bool pdl_on();
+// device check of the quotient helpers (bsq_check.cu; host arrays)
+int check_quotients(int op, const double *x, const double *d, long n, double *out);
 
 // <<<g, b, smem, st>>> with the programmatic-stream-serialization attribute
 // when pdl_on(): the kernel must call pdl_wait() before reading what earlier

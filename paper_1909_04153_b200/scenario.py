@@ -126,13 +126,18 @@ def make_case(name: str, gpus: int = 1, scale: int = 1) -> Case:
         bathy = build_bathymetry(grid, bed, ws=0.0)
         state = solitary_wave_ic(SolitaryWaveSpec(0.0576, 0.32, crest_x=33.0), bathy)
         return Case(name, bathy, state, _walls(), PhysParams(), 0.002, h_dry=1e-3)
-    if name == "C3":
+    if name in ("C3", "C3J"):
+        # C3J: the irregular (JONSWAP) variant of the shoal
         n = 1024 // scale
         grid = Grid(n, n, 0.025 * scale, 0.025 * scale)
         bathy = build_bathymetry(grid, berkhoff_bed(grid), ws=0.0)
         d_west = float(bathy.depth[GHOST:-GHOST, GHOST].min())
-        bounds = bc.Boundaries(west=bc.SineMaker((bc.sine_component(0.0232, 1.0, d_west),)),
-                               east=bc.Sponge(2.0, 10.0), south=bc.Sponge(1.0, 10.0),
+        if name == "C3J":
+            west = bc.IrregularMaker(tuple(bc.jonswap_components(
+                bc.SpectrumSpec(0.05, 1.0, 64, 2.0 / 64, 0), d_west)))
+        else:
+            west = bc.SineMaker((bc.sine_component(0.0232, 1.0, d_west),))
+        bounds = bc.Boundaries(west=west, east=bc.Sponge(2.0, 10.0), south=bc.Sponge(1.0, 10.0),
                                north=bc.Sponge(1.0, 10.0))
         return Case(name, bathy, still_state(bathy), bounds, PhysParams(), 0.002)
     if name in ("C4", "C5"):
