@@ -84,7 +84,11 @@ typedef struct {
     int32_t south_internal, north_internal;
     int32_t row0, ny_global;
     int32_t y_coupling;        /* BSQ_Y_PIPELINE or BSQ_Y_SPIKE (strips only) */
-    int32_t pad_;
+    /* 1: every quotient exact for numerators under 2^-960 as well (the line
+     * solves and k_final divide with the IEEE division; see bsq_device.cuh
+     * "Tiny numerators"); 0: Markstein quotients there, which can miss IEEE
+     * by an ulp for such numerators (the stage is exact either way) */
+    int32_t exact_tiny;
 } bsq_desc;
 
 /* Static fields (host pointers, reference layout; copied at create).  For a
@@ -283,7 +287,8 @@ int bsq_kernels_per_step(bsq_ctx *ctx);
 /* -- test seam: the device quotient helpers on host arrays ----------------
  * out[i] = x[i] / d[i] as computed by helper `op` (bsq_check.cu): 0
  * div_static, 1 div_pos, 2 div_rcp, 3 div_rcp_pos, 4 div_nonneg, 5
- * div_static_pos, 6 the hardware IEEE division.  fp64. */
+ * div_static_pos, 6 the IEEE division, 7 div_tiny_exact (numerators under
+ * 2^-960).  fp64. */
 int bsq_check_quotients(int op, const double *x, const double *d, long n, double *out);
 
 #ifdef __cplusplus

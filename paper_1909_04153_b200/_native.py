@@ -37,7 +37,7 @@ class Desc(ctypes.Structure):
                 ("h_dry", ctypes.c_double), ("ws", ctypes.c_double),
                 ("south_internal", ctypes.c_int32), ("north_internal", ctypes.c_int32),
                 ("row0", ctypes.c_int32), ("ny_global", ctypes.c_int32),
-                ("y_coupling", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+                ("y_coupling", ctypes.c_int32), ("exact_tiny", ctypes.c_int32)]
 
 
 class Static(ctypes.Structure):

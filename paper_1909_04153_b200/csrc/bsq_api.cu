@@ -201,6 +201,7 @@ struct Engine : EngineBase {
     char *base = nullptr;
     DevParams *dparams = nullptr;
     DevResult *dres = nullptr;
+    bool solve_exact = false;  // the line solves divide exactly (EXD): exact_tiny
     Partial *part = nullptr;
     unsigned int *counter = nullptr;
     DevParams *hparams = nullptr;  // pinned
@@ -378,6 +379,21 @@ struct Engine : EngineBase {
         if (p->south_internal) C.side_kind[SIDE_S] = KIND_INTERNAL;
         if (p->north_internal) C.side_kind[SIDE_N] = KIND_INTERNAL;
         C.cross = p->cross_correction;
+    }
+
+    // Whether a static numerator of the stage / correction quotients --
+    // depth (d / 6), d * d_x and d * d_y (/ 3) -- lies under the Markstein
+    // exact range (0 < |x| < 2^-960): then every tile divides exactly.
+    bool static_tiny(const bsq_static *f) const {
+        const long nxt = d.nx + 4;
+        auto tiny = [](double v) { return v != 0.0 && std::fabs(v) < TINY_NUM; };
+        for (int j = 2; j < d.ny + 2; j++)
+            for (int i = 2; i < d.nx + 2; i++) {
+                const long o = j * nxt + i;
+                const double dd = f->depth[o];
+                if (tiny(dd) || tiny(dd * f->depth_dx[o]) || tiny(dd * f->depth_dy[o])) return true;
+            }
+        return false;
     }
 
     // Pre-factor every x row and y column of the static implicit operator
@@ -687,6 +703,9 @@ struct Engine : EngineBase {
             CU(cudaMallocHost(&hframe, sizeof(T) * frame_elems(d.nx, d.ny)));
         }
         set_consts();
+        C.exact = F64 && static_tiny(f) ? 1 : 0;
+        solve_exact = F64 && d.exact_tiny != 0;
+        C.exact_final = solve_exact ? 1 : 0;
         const int nx = d.nx, ny = d.ny;
         CU(cudaMemsetAsync(workspace, 0, need, st));  // ghost cells of scratch arrays stay defined
         int rc;
@@ -889,6 +908,7 @@ struct Engine : EngineBase {
 
     SolvePtrs<T> solve_ptrs(int nxt_state) {
         SolvePtrs<T> S;
+        S.exact = solve_exact;
         S.gp = Pp(nxt_state);
         S.gq = Qq(nxt_state);
         S.cx_last = cx_last;
@@ -1677,7 +1697,7 @@ int bsq_kernel_times(bsq_ctx *c, int max_n, float *ms, const char **names, int *
 }
 
 int bsq_check_quotients(int op, const double *x, const double *d, long n, double *out) {
-    if (!x || !d || !out || n < 0 || op < 0 || op > 6) return fail(BSQ_ERR_BAD_ARG, "bad arguments");
+    if (!x || !d || !out || n < 0 || op < 0 || op > 7) return fail(BSQ_ERR_BAD_ARG, "bad arguments");
     if (n == 0) return BSQ_OK;
     return check_quotients(op, x, d, n, out) ? fail(BSQ_ERR_CUDA, "quotient check failed") : BSQ_OK;
 }

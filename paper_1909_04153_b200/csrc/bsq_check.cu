@@ -26,6 +26,7 @@ __global__ void k_quot(int op, const double *x, const double *d, long n, double 
     case 3: q = div_rcp_pos(a, b, rcp_depth(b)); break;  // flux depths (FAST path)
     case 4: q = div_nonneg(a, b, -rcp_depth(b)); break;  // k_final depths
     case 5: q = div_static_pos(a, b, -rcp_rn(b)); break; // Thomas pivots > 0
+    case 7: q = div_tiny_exact(a, b, rcp_rn(b)); break;  // tiny numerators, call-free
     default: q = a / b; break;                           // IEEE division
     }
     out[i] = q;

@@ -23,7 +23,8 @@ namespace bsq {
 template <class T>
 __host__ __device__ constexpr int cr_rows() { return sizeof(T) == 8 ? BSQ_CORRECT_CR64 : BSQ_CORRECT_CR32; }
 
-template <class T>
+// EXACT: some depth is under Markstein's exact range (Consts::exact, host-checked)
+template <class T, bool EXACT>
 __global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) {
     constexpr int CR = cr_rows<T>();
     pdl_trigger();
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(256) k_correct(Consts<T> C, CorrectPtrs<T> K) 
             T p_y = (pn[1] - ps[1]) * T(0.5) * C.inv_dy;
             T p_xy = (pn[2] - pn[0] - ps[2] + ps[0]) * T(0.25) * C.inv_dx * C.inv_dy;
             T sixth = div_pos(d[k], C.six, C.r_six);
+            if (EXACT && tiny_nz(d[k], TINY_NUM)) sixth = div_tiny_exact(d[k], C.six, C.r_six);
             T d2 = C.bp13 * d[k] * d[k];
             f = sixth * (dx_[k] * q_y + dy_[k] * q_x) + d2 * q_xy;
             g = sixth * (dx_[k] * p_y + dy_[k] * p_x) + d2 * p_xy;
@@ -103,7 +105,7 @@ void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st
         Cb.L.ny = nrows;
     }
     dim3 grid((C.L.nx + 31) / 32, (nrows + 8 * CR - 1) / (8 * CR));  // 32 x (8*CR) cells
-    launch_k(k_correct<T>, grid, dim3(32, 8), 0, st, Cb, Kb);
+    launch_k(Cb.exact ? k_correct<T, true> : k_correct<T, false>, grid, dim3(32, 8), 0, st, Cb, Kb);
 }
 
 #if BSQ_INST_F64

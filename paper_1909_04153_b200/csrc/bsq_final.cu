@@ -123,7 +123,7 @@ __device__ __forceinline__ Red red_block(Red r) {
 
 // speed_extrema contribution of one cell (_kernels.py:337-352); the serial
 // scan's `if x > max` skips NaN, hence the !(x > 0) guards.
-template <bool FAST = false, class T>
+template <bool FAST = false, bool EXT = false, class T>
 __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, T be, Acc<T> &r) {
     // a dry, still cell (h = 0, P = Q = 0) contributes rate = speed = depth = 0,
     // which never raises a maximum: skip it (whole dry warps branch over)
@@ -135,8 +135,13 @@ __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, 
     // both quotients correctly rounded via one reciprocal (branch-free when
     // h_eps is in rcp_rn_inrange's range: bsq_device.cuh flux_fast_rcp_ok)
     const T nrh = -(FAST ? rcp_depth(hstar) : rcp_rn(hstar));
-    const T su = div_nonneg(fabs(p), hstar, nrh) + c;
-    const T sv = div_nonneg(fabs(q), hstar, nrh) + c;
+    T su = div_nonneg(fabs(p), hstar, nrh) + c;
+    T sv = div_nonneg(fabs(q), hstar, nrh) + c;
+    if (EXT && (tiny_nz(p, TINY_NUM) | tiny_nz(q, TINY_NUM))) {  // exact_tiny: under Markstein's range
+        const T rh = -nrh;
+        if (tiny_nz(p, TINY_NUM)) su = div_tiny_exact(fabs(p), hstar, rh) + c;
+        if (tiny_nz(q, TINY_NUM)) sv = div_tiny_exact(fabs(q), hstar, rh) + c;
+    }
     const T rate = nb_max(su * C.inv_dx, sv * C.inv_dy);
     const T speed = nb_max(su, sv);
     if (rate > r.rate) r.rate = rate;
@@ -252,7 +257,7 @@ static __device__ void spec_next(const DevParams &P, double max_rate, DevParams 
 // fixed grid-stride order and reduces once at the end (one block reduction,
 // partial and counter per CTA instead of per tile: the per-tile barrier and
 // atomic were the kernel's top stall after the loads).
-template <class T, bool SPIKE, bool FAST>
+template <class T, bool SPIKE, bool FAST, bool EXT>
 __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, FinalPtrs<T> F,
                                                               int tiles_x, int ntiles) {
     __shared__ bool am_last;
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, Final
                 if (!isfinite(p)) atomicMin(&F.res->state_bad[1], lin);
                 if (!isfinite(q)) atomicMin(&F.res->state_bad[2], lin);
             }
-            extrema_cell<FAST>(C, w, p, q, be, r);
+            extrema_cell<FAST, EXT>(C, w, p, q, be, r);
         }
     }
     }  // tiles
@@ -443,8 +448,11 @@ void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st) {
     const dim3 tg = final_grid(C.L.nx, C.L.ny), blk(FX, FY);
     const int ntiles = (int)(tg.x * tg.y);
     const bool fast = flux_fast_rcp_ok(C.h_eps);
-    auto kern = F.spbt ? (fast ? k_final<T, true, true> : k_final<T, true, false>)
-                       : (fast ? k_final<T, false, true> : k_final<T, false, false>);
+    auto kern = C.exact_final
+                    ? (F.spbt ? (fast ? k_final<T, true, true, true> : k_final<T, true, false, true>)
+                              : (fast ? k_final<T, false, true, true> : k_final<T, false, false, true>))
+                    : (F.spbt ? (fast ? k_final<T, true, true, false> : k_final<T, true, false, false>)
+                              : (fast ? k_final<T, false, true, false> : k_final<T, false, false, false>));
     static int resident = 0;  // CTAs of k_final resident on the device (all four share one shape)
     if (!resident) {
         int dev = 0, sms = 0, per = 0;

@@ -56,6 +56,7 @@ struct SolvePtrs {
     T *dw_out;                      // forward: dw of this strip's last row
     const T *x_in;                  // backward: x of the row above (north rank)
     T *x_out;                       // backward: x of this strip's first row
+    int exact;                      // divide exactly (EXD): exact_tiny requested
 };
 
 // which parts of the line solves a launch runs

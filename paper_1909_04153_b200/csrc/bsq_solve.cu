@@ -81,7 +81,7 @@ __device__ __forceinline__ int toff(int ln, int k) {
 // RDEN_ONCHIP: RN(1/den) is recomputed in the consumer (3 streamed operands
 // instead of 4; 0.347 -> 0.310 ms per solve at 4096^2) whenever every pivot's
 // exponent is within +-1000 (PIV_RDEN_INRANGE, checked at factor time)
-template <class T, bool XDIR, bool POS, bool RDEN_ONCHIP>
+template <class T, bool XDIR, bool POS, bool RDEN_ONCHIP, bool EXD>
 __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
                                 int line0, unsigned char *smem, int mode) {
     using G = TileGeom<T, RDEN_ONCHIP>;
@@ -158,7 +158,11 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
         // from HBM, or (RDEN_ONCHIP) recomputed here off the recurrence's
         // critical path with the branch-free reciprocal (every pivot's exponent
         // is within +-1000, checked at factor time)
+        // EXD (Simulator(exact_subnormal=True) or an operator the host cannot
+        // vouch for): the IEEE division, exact for numerators under 2^-960 too,
+        // where the Markstein step can miss by an ulp (bsq_device.cuh)
         auto step = [&](T num, T den, T nr) -> T {
+            if (EXD) return num / den;
             return POS ? div_static_pos(num, den, nr) : div_static(num, den, -nr);
         };
         auto nrden = [&](const T *st, int t) -> T {
@@ -304,7 +308,7 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
 }
 
 // Blocks [0, nbx) take x lines (rows -> P); blocks [nbx, ...) y lines (columns -> Q).
-template <class T, bool POS, bool ONCHIP>
+template <class T, bool POS, bool ONCHIP, bool EXD>
 __global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_constant__ SolveMaps M,
                                                   SolvePtrs<T> S, int nbx, int mode) {
     extern __shared__ unsigned char smem_raw[];
@@ -313,9 +317,9 @@ __global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_cons
     pdl_trigger();
     pdl_wait();
     if ((int)blockIdx.x < nbx)
-        solve_lines_tma<T, true, POS, ONCHIP>(C, M, S, blockIdx.x * NLINE, smem, mode);
+        solve_lines_tma<T, true, POS, ONCHIP, EXD>(C, M, S, blockIdx.x * NLINE, smem, mode);
     else
-        solve_lines_tma<T, false, POS, ONCHIP>(C, M, S, (blockIdx.x - nbx) * NLINE, smem, mode);
+        solve_lines_tma<T, false, POS, ONCHIP, EXD>(C, M, S, (blockIdx.x - nbx) * NLINE, smem, mode);
 }
 
 // pos_pivots: every Thomas pivot of both operators is > 0 (host-checked), which
@@ -328,10 +332,11 @@ void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
     const int smem_on = TileGeom<T, true>::SMEM_B, smem_off = TileGeom<T, false>::SMEM_B;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_solve_tma<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_on);
-        cudaFuncSetAttribute(k_solve_tma<T, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_on);
-        cudaFuncSetAttribute(k_solve_tma<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_off);
-        cudaFuncSetAttribute(k_solve_tma<T, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_off);
+        cudaFuncSetAttribute(k_solve_tma<T, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_on);
+        cudaFuncSetAttribute(k_solve_tma<T, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_on);
+        cudaFuncSetAttribute(k_solve_tma<T, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_off);
+        cudaFuncSetAttribute(k_solve_tma<T, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_off);
+        cudaFuncSetAttribute(k_solve_tma<T, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_off);
         attr_set = true;
     }
     const int bx = mode == SOLVE_YBWD ? 0 : nbx;  // x-line CTAs in this launch
@@ -342,14 +347,16 @@ void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
     const bool onchip = pivots & PIV_RDEN_INRANGE;
 #endif
     dim3 g(bx + nby), b(64);
-    if (pos && onchip)
-        launch_k(k_solve_tma<T, true, true>, g, b, smem_on, st, C, M, S, bx, mode);
+    if (S.exact)
+        launch_k(k_solve_tma<T, false, false, true>, g, b, smem_off, st, C, M, S, bx, mode);
+    else if (pos && onchip)
+        launch_k(k_solve_tma<T, true, true, false>, g, b, smem_on, st, C, M, S, bx, mode);
     else if (pos)
-        launch_k(k_solve_tma<T, true, false>, g, b, smem_off, st, C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, true, false, false>, g, b, smem_off, st, C, M, S, bx, mode);
     else if (onchip)
-        launch_k(k_solve_tma<T, false, true>, g, b, smem_on, st, C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, false, true, false>, g, b, smem_on, st, C, M, S, bx, mode);
     else
-        launch_k(k_solve_tma<T, false, false>, g, b, smem_off, st, C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, false, false, false>, g, b, smem_off, st, C, M, S, bx, mode);
 }
 
 #if BSQ_INST_F64

@@ -25,6 +25,7 @@
 // in three rounds, so no warp mixes item kinds and no index needs a divide.
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include "bsq_device.cuh"
 #include "bsq_launch.h"
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         S.f.ylo[2][r][c] = f.qlo;
     };
     static_assert(TX == 32 && TY >= 4 && TY <= 16, "2-D item maps: warp = tile row, 32 columns");
+    bool tiny = false;
     xface(ty, tx);
     yface(ty, tx);
     if (ty < 2) {
@@ -170,12 +172,21 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     } else if (ty == 2) {
         if (tx < 2 * TY) xface(tx >> 1, TX + (tx & 1));
     } else {
-        // eta = (w - bed_eff) - depth over the halo box (dispersion.py:87)
-        for (int k = tid - 3 * TX; k < HY * HX; k += NT - 3 * TX)
+        // eta = (w - bed_eff) - depth over the halo box (dispersion.py:87);
+        // the same warps look for tiny momenta in the box (0 < |P|,|Q| <
+        // 2^-400), which could put a numerator under Markstein's exact range
+        for (int k = tid - 3 * TX; k < HY * HX; k += NT - 3 * TX) {
             (&S.eta[0][0])[k] = ((&S.w[0][0])[k] - (&S.be[0][0])[k]) - (&S.dep[0][0])[k];
+            tiny |= tiny_nz((&S.p[0][0])[k], TINY_IN) | tiny_nz((&S.q[0][0])[k], TINY_IN);
+        }
     }
-    __syncthreads();
+    // the tile divides exactly (IEEE) if any input was tiny: rare, warp-uniform
+    const bool exact = __syncthreads_or(tiny | C.exact) != 0;
 
+    // phases C and D, instantiated twice: the Markstein quotients, or (a tile
+    // with tiny inputs, never on ordinary data) IEEE divisions throughout
+    auto phase_cd = [&](auto ex_tag) {
+    constexpr bool EX = decltype(ex_tag)::value;
     // ---- C: fluxes, written over the faces they consume --------------------------
     //   round 0  x interfaces of row ty, 0..31;  round 1  y interface row ty
     //   round 2  warp 0: y interface row 8; warp 1: x interface 32 of the 8 rows
@@ -186,7 +197,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     // between computing and storing.  Same for y with row yi's north faces.
     auto xflux = [&](int r, int xi) {
         T f1, f2, f3;
-        cu_flux_rcp<FR>(S.f.xhi[0][r][xi], S.f.xlo[0][r][xi + 1], S.f.xhi[1][r][xi],
+        cu_flux_rcp<FR, EX>(S.f.xhi[0][r][xi], S.f.xlo[0][r][xi + 1], S.f.xhi[1][r][xi],
                     S.f.xlo[1][r][xi + 1], S.f.xhi[2][r][xi], S.f.xlo[2][r][xi + 1],
                     S.bfx[r][xi + 1], C.g, C.half_g, C.h_eps, f1, f2, f3);
         S.f.xhi[0][r][xi] = f1;
@@ -195,7 +206,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     };
     auto yflux = [&](int yi, int c) {  // south cell = face row yi; normal = Q
         T f1, fq, fp;
-        cu_flux_rcp<FR>(S.f.yhi[0][yi][c], S.f.ylo[0][yi + 1][c], S.f.yhi[2][yi][c],
+        cu_flux_rcp<FR, EX>(S.f.yhi[0][yi][c], S.f.ylo[0][yi + 1][c], S.f.yhi[2][yi][c],
                     S.f.ylo[2][yi + 1][c], S.f.yhi[1][yi][c], S.f.ylo[1][yi + 1][c],
                     S.bfy[yi + 1][c], C.g, C.half_g, C.h_eps, f1, fq, fp);
         S.f.yhi[0][yi][c] = f1;
@@ -232,7 +243,8 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     T fric = T(0);
     if (C.c_f > T(0)) {  // c_f sqrt(P^2 + Q^2) / h*^2, the quotient via RN(1/h*^2) (div_rcp)
         const T h2 = hstar * hstar;
-        fric = div_rcp(C.c_f * sqrt(pc * pc + qc * qc), h2, rcp_rn(h2));
+        const T num = C.c_f * sqrt(pc * pc + qc * qc);
+        fric = qx<EX>(div_rcp(num, h2, rcp_rn(h2)), num, h2);
     }
     T rp = -(FX(1, ty, tx + 1) - FX(1, ty, tx)) * C.inv_dx -
            (FY(1, ty + 1, tx) - FY(1, ty, tx)) * C.inv_dy + src_x - fric * pc;
@@ -273,7 +285,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         const T p_y = (S.p[y + 1][x] - S.p[y - 1][x]) * T(0.5) * C.inv_dy;
         const T p_xy = (S.p[y + 1][x + 1] - S.p[y + 1][x - 1] - S.p[y - 1][x + 1] +
                         S.p[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
-        const T sixth = div_pos(d, C.six, C.r_six);
+        const T sixth = qx<EX>(div_pos(d, C.six, C.r_six), d, C.six);
         const T d2 = C.bp13 * d * d;
         fs_ = sixth * (dx_ * q_y + dy_ * q_x) + d2 * q_xy;
         gs_ = sixth * (dx_ * p_y + dy_ * p_x) + d2 * p_xy;
@@ -300,12 +312,16 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     if (!predict) return;
 
     // U*, V* (dispersion.py:131-148): divisions by grid constants
-    const T p_x = div_pos(S.p[y][x + 1] - S.p[y][x - 1], C.two_dx, C.r_two_dx);
-    const T p_xx = div_pos(S.p[y][x + 1] - T(2) * pc + S.p[y][x - 1], C.dx2, C.r_dx2);
-    const T ustar = pc - div_pos(d * dx_, C.three, C.r_three) * p_x - C.bp13 * d * d * p_xx;
-    const T q_y = div_pos(S.q[y + 1][x] - S.q[y - 1][x], C.two_dy, C.r_two_dy);
-    const T q_yy = div_pos(S.q[y + 1][x] - T(2) * qc + S.q[y - 1][x], C.dy2, C.r_dy2);
-    const T vstar = qc - div_pos(d * dy_, C.three, C.r_three) * q_y - C.bp13 * d * d * q_yy;
+    const T pdx = S.p[y][x + 1] - S.p[y][x - 1], pdxx = S.p[y][x + 1] - T(2) * pc + S.p[y][x - 1];
+    const T p_x = qx<EX>(div_pos(pdx, C.two_dx, C.r_two_dx), pdx, C.two_dx);
+    const T p_xx = qx<EX>(div_pos(pdxx, C.dx2, C.r_dx2), pdxx, C.dx2);
+    const T ddx3 = d * dx_;
+    const T ustar = pc - qx<EX>(div_pos(ddx3, C.three, C.r_three), ddx3, C.three) * p_x - C.bp13 * d * d * p_xx;
+    const T qdy = S.q[y + 1][x] - S.q[y - 1][x], qdyy = S.q[y + 1][x] - T(2) * qc + S.q[y - 1][x];
+    const T q_y = qx<EX>(div_pos(qdy, C.two_dy, C.r_two_dy), qdy, C.two_dy);
+    const T q_yy = qx<EX>(div_pos(qdyy, C.dy2, C.r_dy2), qdyy, C.dy2);
+    const T ddy3 = d * dy_;
+    const T vstar = qc - qx<EX>(div_pos(ddy3, C.three, C.r_three), ddy3, C.three) * q_y - C.bp13 * d * d * q_yy;
 
     // predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
     T wn, bu, bv, us, vs;
@@ -330,6 +346,9 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     A.bv[o] = bv;
     A.us[o] = us;
     A.vs[o] = vs;
+    };
+    if (exact) phase_cd(std::true_type{});
+    else phase_cd(std::false_type{});
 }
 
 }  // namespace tiled

@@ -168,16 +168,21 @@ class Simulator:
     """Adaptive-AB3 Boussinesq simulation whose per-step work runs on a B200.
 
     Constructor, ``advance``/``run`` and attributes as the reference
-    (stepper.py:170-340).  Extra keywords: ``device`` (torch device spec) and
+    (stepper.py:170-340).  Extra keywords: ``device`` (torch device spec),
     ``precision``: "fp64" (default; bitwise equal to the reference) or "fp32"
-    (device storage and arithmetic in float; host API stays float64).
+    (device storage and arithmetic in float; host API stays float64), and
+    ``exact_subnormal``: the line solves and the CFL extrema also divide
+    numerators under 2^-960 (values below ~1e-289, e.g. a far field decayed
+    into the subnormal range) with IEEE rounding.  Off, those quotients are
+    Markstein's and can miss IEEE's by an ulp; the stage is exact either way
+    (bsq_device.cuh "Tiny numerators"; tests/test_gpu_tiny.py).
     """
 
     def __init__(self, bathy, state, boundaries, controller,
                  numerics: NumericsParams | None = None, phys: PhysParams | None = None,
                  solver: str = "thomas", blowup_bound: float | None = None,
                  cross_correction: bool = True, h_dry: float | None = None,
-                 device=None, precision: str = "fp64"):
+                 device=None, precision: str = "fp64", exact_subnormal: bool = False):
         self.bathy = bathy
         self.boundaries = boundaries
         self.controller = controller
@@ -204,6 +209,7 @@ class Simulator:
         d.precision = nat.FP64 if precision == "fp64" else nat.FP32
         d.solver = nat.THOMAS if solver == "thomas" else nat.CR
         d.cross_correction = 1 if cross_correction else 0
+        d.exact_tiny = 1 if exact_subnormal else 0
         self._bands = [None] * 4
         for k, (side, pol, kind) in enumerate(zip(bc.SIDES, self._policies, self._kinds)):
             d.side_kind[k] = _KIND_CODE[kind]
