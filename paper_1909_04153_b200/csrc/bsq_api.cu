@@ -586,12 +586,13 @@ struct Engine : EngineBase {
         return BSQ_OK;
     }
 
-    // stage tile boxes: 36 x 12 (32 x 8 tile + 2-cell halo; fp32 boxes are
-    // only built, the fp32 stage is the column walk)
+    // stage tile boxes: 36 x 12 (32 x 8 tile + 2-cell halo); fp32: 40 x 12,
+    // starting two columns further west (box origins on 16-B boundaries:
+    // bsq_stage_tiled.cu Box<T>)
     CUtensorMap smap_w[3], smap_p[2], smap_q[2], smap_be, smap_dep, smap_bfx, smap_bfy;
     int build_stage_maps() {
-        const int nxt = d.nx + 4, nyt = d.ny + 4, TX = STAGE_TX, TY = STAGE_TY, HX = TX + 4,
-                  HY = TY + 4;
+        const int nxt = d.nx + 4, nyt = d.ny + 4, TX = STAGE_TX, TY = STAGE_TY,
+                  HX = TX + (F64 ? 4 : 8), HY = TY + 4;
         int rc;
         for (int k = 0; k < 3; k++)
             if ((rc = make_map_box(&smap_w[k], arr[kW[k]], nxt, nyt, HX, HY))) return rc;

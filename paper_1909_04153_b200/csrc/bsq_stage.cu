@@ -351,17 +351,22 @@ template <class T>
 void launch_stage_tiled(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
                         cudaStream_t st, const StageMaps *M, int row0, int nrows);
 
-// fp64 runs the tiled variant (bsq_stage_tiled.cu: 64 registers, 32 warps per
-// SM) -- the column walk needs 128 fp64 registers and loses on latency hiding
-// (1.317 vs 1.114 ms at 4096^2); fp32 runs the column walk (72 registers;
-// tiled 0.821 vs 0.722 ms).  Measured A/B on B200, round 1.
+// Both precisions run the tiled variant (bsq_stage_tiled.cu; fp64: 64
+// registers, 32 warps per SM -- the column walk below needs 128 fp64
+// registers and loses on latency hiding, 1.317 vs 1.114 ms at 4096^2; fp32:
+// 0.473 vs 0.593 ms for the column walk once the fp32 boxes start on 16-B
+// boundaries).  BSQ_F32_TILED=0 selects the fp32 column walk (A/B only).
 template <class T>
 void launch_stage(const Consts<T> &C, const DevParams *P, const StagePtrs<T> &A, int predict,
                   cudaStream_t st, const StageMaps *M, int row0, int nrows) {
     static_assert(STAGE_BAND % STY == 0 && STAGE_BAND % STAGE_TY == 0, "band of whole tiles");
     if (nrows < 0) nrows = C.L.ny - row0;
     if (nrows <= 0) return;
-    if constexpr (sizeof(T) == 8) {
+    static const bool f32_tiled = [] {
+        const char *e = std::getenv("BSQ_F32_TILED");
+        return !(e && e[0] == '0');
+    }();
+    if (sizeof(T) == 8 || f32_tiled) {
         launch_stage_tiled(C, P, A, predict, st, M, row0, nrows);
     } else {
         const size_t smem = sizeof(StageSmem<T>);

@@ -46,20 +46,30 @@ constexpr int NXI = TY * (TX + 1), NYI = (TY + 1) * TX;  // interface items
 constexpr int NFL = NXI + NYI;
 constexpr int FL_PASSES = (NFL + NT - 1) / NT;
 
-// TMA boxes need 16-byte multiples along x: the bed_face_x box is HX wide
-// (one column more than used)
-constexpr int BFXW = HX;
+// TMA tile loads need the box origin on a 16-byte boundary along x (measured:
+// tools/tma_box_probe.cu, an "illegal instruction" otherwise) and box widths
+// of 16-byte multiples.  The halo box starts at padded column I0 - 2: 16-B
+// aligned in fp64 (xo = 14), 8 B off in fp32 (xo = 30), where the boxes start
+// XS = 2 columns further west and are 40 wide; smem column c of the tile's
+// view is box column c + XS.
+template <class T>
+struct Box {
+    static constexpr int XS = sizeof(T) == 8 ? 0 : 2;
+    static constexpr int W = sizeof(T) == 8 ? HX : HX + 4;  // loaded width (bed_face_x too:
+                                                            // one column more than used)
+};
 
 template <class T>
 struct StageSmem {
+    static constexpr int W = Box<T>::W;
     // TMA destinations: 128-byte aligned each
-    alignas(128) T w[HY][HX];
-    alignas(128) T p[HY][HX];
-    alignas(128) T q[HY][HX];
-    alignas(128) T be[HY][HX];
-    alignas(128) T dep[HY][HX];
-    alignas(128) T eta[HY][HX];
-    alignas(128) T bfx[TY][BFXW];    // bed_face_x for columns -2..TX
+    alignas(128) T w[HY][W];
+    alignas(128) T p[HY][W];
+    alignas(128) T q[HY][W];
+    alignas(128) T be[HY][W];
+    alignas(128) T dep[HY][W];
+    alignas(128) T eta[HY][W];
+    alignas(128) T bfx[TY][W];    // bed_face_x for columns -2..TX
     alignas(128) T bfy[TY + 3][TX];  // bed_face_y for rows -2..TY
     alignas(8) uint64_t bar;
     struct {  // phase B/C faces (hi = east/north, lo = west/south; w, P, Q);
@@ -95,11 +105,12 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         fence_mbar_init();
     }
     __syncthreads();
+    constexpr int XS = Box<T>::XS, BW = Box<T>::W;
     if (tid == 0) {
-        // halo box origin: padded column I0 - 2 (+ xo: the maps start at the
-        // pitched row), padded row J0 - 2
-        const int x0 = L.xo + I0 - GL, y0 = J0 - GL;
-        mbar_expect_tx(&S.bar, (unsigned)sizeof(T) * (5 * HY * HX + TY * BFXW + (TY + 3) * TX));
+        // halo box origin: padded column I0 - 2 - XS (+ xo: the maps start at
+        // the pitched row), padded row J0 - 2
+        const int x0 = L.xo + I0 - GL - XS, y0 = J0 - GL;
+        mbar_expect_tx(&S.bar, (unsigned)sizeof(T) * (5 * HY * BW + TY * BW + (TY + 3) * TX));
         tma_load_2d(&S.w[0][0], &M.w, x0, y0, &S.bar);
         tma_load_2d(&S.p[0][0], &M.p, x0, y0, &S.bar);
         tma_load_2d(&S.q[0][0], &M.q, x0, y0, &S.bar);
@@ -108,6 +119,14 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         tma_load_2d(&S.bfx[0][0], &M.bfx, x0, J0, &S.bar);
         tma_load_2d(&S.bfy[0][0], &M.bfy, L.xo + I0, y0, &S.bar);
     }
+    // the tile's views: column 0 = padded column I0 - 2
+    T(*const Sw)[BW] = reinterpret_cast<T(*)[BW]>(&S.w[0][XS]);
+    T(*const Sp)[BW] = reinterpret_cast<T(*)[BW]>(&S.p[0][XS]);
+    T(*const Sq)[BW] = reinterpret_cast<T(*)[BW]>(&S.q[0][XS]);
+    T(*const Sbe)[BW] = reinterpret_cast<T(*)[BW]>(&S.be[0][XS]);
+    T(*const Sdep)[BW] = reinterpret_cast<T(*)[BW]>(&S.dep[0][XS]);
+    T(*const Seta)[BW] = reinterpret_cast<T(*)[BW]>(&S.eta[0][XS]);
+    T(*const Sbfx)[BW] = reinterpret_cast<T(*)[BW]>(&S.bfx[0][XS]);
     // phase D's per-cell inputs that phase A does not read: start them towards
     // L2 now (no registers held), so phase D's loads hit on chip
 #ifndef BSQ_STAGE_LANE_PREFETCH
@@ -141,9 +160,9 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     //            the 8 rows (16 lanes); warps 3..7: eta over the halo box
     auto xface = [&](int r, int c) {  // x faces of cell (row r, column c-1)
         const int y = r + 2, x = c + 1;
-        const Faces<T> f = cell_faces(S.w[y][x - 1], S.w[y][x], S.w[y][x + 1], S.p[y][x - 1],
-                                      S.p[y][x], S.p[y][x + 1], S.q[y][x - 1], S.q[y][x],
-                                      S.q[y][x + 1], S.bfx[r][c + 1], S.bfx[r][c], C.theta);
+        const Faces<T> f = cell_faces(Sw[y][x - 1], Sw[y][x], Sw[y][x + 1], Sp[y][x - 1],
+                                      Sp[y][x], Sp[y][x + 1], Sq[y][x - 1], Sq[y][x],
+                                      Sq[y][x + 1], Sbfx[r][c + 1], Sbfx[r][c], C.theta);
         S.f.xhi[0][r][c] = f.whi;
         S.f.xlo[0][r][c] = f.wlo;
         S.f.xhi[1][r][c] = f.phi;
@@ -153,9 +172,9 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     };
     auto yface = [&](int r, int c) {  // y faces of cell (row r-1, column c)
         const int y = r + 1, x = c + 2;
-        const Faces<T> f = cell_faces(S.w[y - 1][x], S.w[y][x], S.w[y + 1][x], S.p[y - 1][x],
-                                      S.p[y][x], S.p[y + 1][x], S.q[y - 1][x], S.q[y][x],
-                                      S.q[y + 1][x], S.bfy[r + 1][c], S.bfy[r][c], C.theta);
+        const Faces<T> f = cell_faces(Sw[y - 1][x], Sw[y][x], Sw[y + 1][x], Sp[y - 1][x],
+                                      Sp[y][x], Sp[y + 1][x], Sq[y - 1][x], Sq[y][x],
+                                      Sq[y + 1][x], S.bfy[r + 1][c], S.bfy[r][c], C.theta);
         S.f.yhi[0][r][c] = f.whi;
         S.f.ylo[0][r][c] = f.wlo;
         S.f.yhi[1][r][c] = f.phi;
@@ -175,7 +194,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         // eta = (w - bed_eff) - depth over the halo box (dispersion.py:87);
         // the same warps look for tiny momenta in the box (0 < |P|,|Q| <
         // 2^-400), which could put a numerator under Markstein's exact range
-        for (int k = tid - 3 * TX; k < HY * HX; k += NT - 3 * TX) {
+        for (int k = tid - 3 * TX; k < HY * BW; k += NT - 3 * TX) {
             (&S.eta[0][0])[k] = ((&S.w[0][0])[k] - (&S.be[0][0])[k]) - (&S.dep[0][0])[k];
             tiny |= tiny_nz((&S.p[0][0])[k], TINY_IN) | tiny_nz((&S.q[0][0])[k], TINY_IN);
         }
@@ -199,7 +218,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         T f1, f2, f3;
         cu_flux_rcp<FR, EX>(S.f.xhi[0][r][xi], S.f.xlo[0][r][xi + 1], S.f.xhi[1][r][xi],
                     S.f.xlo[1][r][xi + 1], S.f.xhi[2][r][xi], S.f.xlo[2][r][xi + 1],
-                    S.bfx[r][xi + 1], C.g, C.half_g, C.h_eps, f1, f2, f3);
+                    Sbfx[r][xi + 1], C.g, C.half_g, C.h_eps, f1, f2, f3);
         S.f.xhi[0][r][xi] = f1;
         S.f.xhi[1][r][xi] = f2;
         S.f.xhi[2][r][xi] = f3;
@@ -227,9 +246,9 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     if (J >= ny + GL || I >= nx + GL) return;
     const int y = ty + 2, x = tx + 2;
     const long o = L.at(J, I);
-    const T wc = S.w[y][x], pc = S.p[y][x], qc = S.q[y][x];
+    const T wc = Sw[y][x], pc = Sp[y][x], qc = Sq[y][x];
     if (A.maxw) A.maxw[o] = np_maximum(A.maxw[o], wc);  // MaxSurfaceTracker fold
-    const T be_ = S.bfx[ty][tx + 2], bw_ = S.bfx[ty][tx + 1];
+    const T be_ = Sbfx[ty][tx + 2], bw_ = Sbfx[ty][tx + 1];
     const T bn_ = S.bfy[ty + 2][tx], bs_ = S.bfy[ty + 1][tx];
 
     // fv_rates (_kernels.py:230-251)
@@ -237,7 +256,7 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
            (FY(0, ty + 1, tx) - FY(0, ty, tx)) * C.inv_dy;
     const T src_x = -C.g * (wc - T(0.5) * (be_ + bw_)) * (be_ - bw_) * C.inv_dx;
     const T src_y = -C.g * (wc - T(0.5) * (bn_ + bs_)) * (bn_ - bs_) * C.inv_dy;
-    T h = wc - S.be[y][x];
+    T h = wc - Sbe[y][x];
     h = floor0(h);
     const T hstar = floor_eps(h, C.h_eps);
     T fric = T(0);
@@ -251,24 +270,24 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     T rq = -(FX(2, ty, tx + 1) - FX(2, ty, tx)) * C.inv_dx -
            (FY(2, ty + 1, tx) - FY(2, ty, tx)) * C.inv_dy + src_y - fric * qc;
 
-    const T d = S.dep[y][x], dx_ = A.ddx[o], dy_ = A.ddy[o];
+    const T d = Sdep[y][x], dx_ = A.ddx[o], dy_ = A.ddy[o];
     T fs_, gs_;
     if (d > T(0)) {
         // dispersive_rates (_kernels.py:269-288)
-        const T ec = S.eta[y][x];
-        const T e_xx = (S.eta[y][x + 1] - T(2) * ec + S.eta[y][x - 1]) * C.inv_dx2;
-        const T e_yy = (S.eta[y + 1][x] - T(2) * ec + S.eta[y - 1][x]) * C.inv_dy2;
-        const T e_xy = (S.eta[y + 1][x + 1] - S.eta[y + 1][x - 1] - S.eta[y - 1][x + 1] +
-                        S.eta[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
-        const T e_xxx = (S.eta[y][x + 2] - T(2) * S.eta[y][x + 1] + T(2) * S.eta[y][x - 1] -
-                         S.eta[y][x - 2]) * T(0.5) * C.inv_dx * C.inv_dx2;
-        const T e_yyy = (S.eta[y + 2][x] - T(2) * S.eta[y + 1][x] + T(2) * S.eta[y - 1][x] -
-                         S.eta[y - 2][x]) * T(0.5) * C.inv_dy * C.inv_dy2;
-        const T e_xyy = ((S.eta[y + 1][x + 1] - T(2) * S.eta[y][x + 1] + S.eta[y - 1][x + 1]) -
-                         (S.eta[y + 1][x - 1] - T(2) * S.eta[y][x - 1] + S.eta[y - 1][x - 1])) *
+        const T ec = Seta[y][x];
+        const T e_xx = (Seta[y][x + 1] - T(2) * ec + Seta[y][x - 1]) * C.inv_dx2;
+        const T e_yy = (Seta[y + 1][x] - T(2) * ec + Seta[y - 1][x]) * C.inv_dy2;
+        const T e_xy = (Seta[y + 1][x + 1] - Seta[y + 1][x - 1] - Seta[y - 1][x + 1] +
+                        Seta[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+        const T e_xxx = (Seta[y][x + 2] - T(2) * Seta[y][x + 1] + T(2) * Seta[y][x - 1] -
+                         Seta[y][x - 2]) * T(0.5) * C.inv_dx * C.inv_dx2;
+        const T e_yyy = (Seta[y + 2][x] - T(2) * Seta[y + 1][x] + T(2) * Seta[y - 1][x] -
+                         Seta[y - 2][x]) * T(0.5) * C.inv_dy * C.inv_dy2;
+        const T e_xyy = ((Seta[y + 1][x + 1] - T(2) * Seta[y][x + 1] + Seta[y - 1][x + 1]) -
+                         (Seta[y + 1][x - 1] - T(2) * Seta[y][x - 1] + Seta[y - 1][x - 1])) *
                         T(0.5) * C.inv_dx * C.inv_dy2;
-        const T e_xxy = ((S.eta[y + 1][x + 1] - T(2) * S.eta[y + 1][x] + S.eta[y + 1][x - 1]) -
-                         (S.eta[y - 1][x + 1] - T(2) * S.eta[y - 1][x] + S.eta[y - 1][x - 1])) *
+        const T e_xxy = ((Seta[y + 1][x + 1] - T(2) * Seta[y + 1][x] + Seta[y + 1][x - 1]) -
+                         (Seta[y - 1][x + 1] - T(2) * Seta[y - 1][x] + Seta[y - 1][x - 1])) *
                         T(0.5) * C.inv_dy * C.inv_dx2;
         const T gd2 = C.g * d * d;
         const T gd3 = gd2 * d;
@@ -277,14 +296,14 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
         rq += C.b_disp * gd3 * (e_yyy + e_xxy) +
               C.b_disp * gd2 * (dy_ * (T(2) * e_yy + e_xx) + dx_ * e_xy);
         // cross_rates (_kernels.py:310-321)
-        const T q_x = (S.q[y][x + 1] - S.q[y][x - 1]) * T(0.5) * C.inv_dx;
-        const T q_y = (S.q[y + 1][x] - S.q[y - 1][x]) * T(0.5) * C.inv_dy;
-        const T q_xy = (S.q[y + 1][x + 1] - S.q[y + 1][x - 1] - S.q[y - 1][x + 1] +
-                        S.q[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
-        const T p_x = (S.p[y][x + 1] - S.p[y][x - 1]) * T(0.5) * C.inv_dx;
-        const T p_y = (S.p[y + 1][x] - S.p[y - 1][x]) * T(0.5) * C.inv_dy;
-        const T p_xy = (S.p[y + 1][x + 1] - S.p[y + 1][x - 1] - S.p[y - 1][x + 1] +
-                        S.p[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+        const T q_x = (Sq[y][x + 1] - Sq[y][x - 1]) * T(0.5) * C.inv_dx;
+        const T q_y = (Sq[y + 1][x] - Sq[y - 1][x]) * T(0.5) * C.inv_dy;
+        const T q_xy = (Sq[y + 1][x + 1] - Sq[y + 1][x - 1] - Sq[y - 1][x + 1] +
+                        Sq[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
+        const T p_x = (Sp[y][x + 1] - Sp[y][x - 1]) * T(0.5) * C.inv_dx;
+        const T p_y = (Sp[y + 1][x] - Sp[y - 1][x]) * T(0.5) * C.inv_dy;
+        const T p_xy = (Sp[y + 1][x + 1] - Sp[y + 1][x - 1] - Sp[y - 1][x + 1] +
+                        Sp[y - 1][x - 1]) * T(0.25) * C.inv_dx * C.inv_dy;
         const T sixth = qx<EX>(div_pos(d, C.six, C.r_six), d, C.six);
         const T d2 = C.bp13 * d * d;
         fs_ = sixth * (dx_ * q_y + dy_ * q_x) + d2 * q_xy;
@@ -312,12 +331,12 @@ __global__ void __launch_bounds__(NT, BSQ_STAGE_MINB) k_stage(Consts<T> C, const
     if (!predict) return;
 
     // U*, V* (dispersion.py:131-148): divisions by grid constants
-    const T pdx = S.p[y][x + 1] - S.p[y][x - 1], pdxx = S.p[y][x + 1] - T(2) * pc + S.p[y][x - 1];
+    const T pdx = Sp[y][x + 1] - Sp[y][x - 1], pdxx = Sp[y][x + 1] - T(2) * pc + Sp[y][x - 1];
     const T p_x = qx<EX>(div_pos(pdx, C.two_dx, C.r_two_dx), pdx, C.two_dx);
     const T p_xx = qx<EX>(div_pos(pdxx, C.dx2, C.r_dx2), pdxx, C.dx2);
     const T ddx3 = d * dx_;
     const T ustar = pc - qx<EX>(div_pos(ddx3, C.three, C.r_three), ddx3, C.three) * p_x - C.bp13 * d * d * p_xx;
-    const T qdy = S.q[y + 1][x] - S.q[y - 1][x], qdyy = S.q[y + 1][x] - T(2) * qc + S.q[y - 1][x];
+    const T qdy = Sq[y + 1][x] - Sq[y - 1][x], qdyy = Sq[y + 1][x] - T(2) * qc + Sq[y - 1][x];
     const T q_y = qx<EX>(div_pos(qdy, C.two_dy, C.r_two_dy), qdy, C.two_dy);
     const T q_yy = qx<EX>(div_pos(qdyy, C.dy2, C.r_dy2), qdyy, C.dy2);
     const T ddy3 = d * dy_;
