@@ -96,3 +96,32 @@ def test_default_mode_normal_range_bitwise():
         small = ~big
         if small.any():
             assert np.all(np.abs(got[small]) < 2.0 ** -800), f
+
+
+def test_tiny_momenta_on_y_strips_bitwise():
+    """Emulated y-strips (pipeline coupling, bitwise = one grid): tiny
+    momenta in halo rows that arrive from another strip are detected by the
+    receiving strip's stage tiles too."""
+    from paper_1909_04153_b200 import parallel
+    rng = np.random.default_rng(11)
+    grid = Grid(64, 48, 0.25, 0.25)
+    xc, yc = np.meshgrid(grid.x_centers(), grid.y_centers())
+    bathy = build_bathymetry(grid, -0.6 + 0.2 * np.exp(-((xc - 8) ** 2 + (yc - 6) ** 2) / 3.0),
+                             ws=0.0)
+    st = still_state(bathy)
+    shape = st.w.shape
+    st.w += 0.02 * np.exp(-((np.pad(xc, 2, mode="edge") - 4) ** 2) / 2.0)
+    st.p = 10.0 ** rng.uniform(-320, -290, shape) * rng.choice([-1.0, 1.0], shape)
+    st.q = 10.0 ** rng.uniform(-320, -290, shape) * rng.choice([-1.0, 1.0], shape)
+    phys = PhysParams()
+    sim = parallel.ShardedSimulator(bathy, st.copy(), walls(), stepper.TimeController(dt_init=0.01),
+                                    phys=phys, exact_subnormal=True, world=3, coupling="pipeline")
+    ora = orc.OracleSimulator(bathy, st.copy(), walls(), orc.OController(dt_init=0.01), phys=phys,
+                              threads=4)
+    for k in range(8):
+        a, b = sim.advance(), ora.advance()
+        assert (a.dt, a.max_cfl, a.max_speed, a.max_depth) == \
+            (b.dt, b.max_cfl, b.max_speed, b.max_depth), k
+    for f in ("w", "p", "q"):
+        got, want = getattr(sim.state, f), getattr(ora.state, f)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), f
