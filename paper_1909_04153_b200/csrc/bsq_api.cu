@@ -19,8 +19,29 @@
 
 #include <cudaTypedefs.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/bsq.h"
 #include "bsq_launch.h"
+
+// NVTX ranges around the entry points (header-only NVTX v3: a no-op unless a
+// profiler is attached), so an nsys / ncu timeline shows which call a
+// kernel belongs to
+namespace {
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+const char *phase_name(int ph) {
+    static const char *names[] = {"bsq_phase:ghost",         "bsq_phase:stage",
+                                  "bsq_phase:solve1_fwd",    "bsq_phase:solve1_bwd",
+                                  "bsq_phase:correct",       "bsq_phase:solve2_fwd",
+                                  "bsq_phase:solve2_bwd",    "bsq_phase:final",
+                                  "bsq_phase:stage_inner",   "bsq_phase:stage_edge",
+                                  "bsq_phase:correct_inner", "bsq_phase:correct_edge"};
+    return (ph >= 0 && ph < (int)(sizeof(names) / sizeof(names[0]))) ? names[ph] : "bsq_phase";
+}
+}  // namespace
 
 using namespace bsq;
 
@@ -1582,6 +1603,7 @@ int bsq_download_history(bsq_ctx *c, int level, int field, double *out) {
 }
 
 int bsq_step(bsq_ctx *c, const bsq_step_params *p, bsq_step_result *r) {
+    NvtxRange nv("bsq_step");
     if (!c || !p || !r) return fail(BSQ_ERR_BAD_ARG, "null argument");
     return ENGINE(c, e->step(p, r));
 }
@@ -1592,6 +1614,7 @@ int bsq_commit(bsq_ctx *c) {
 }
 
 int bsq_phase(bsq_ctx *c, int phase, const bsq_step_params *p, bsq_step_result *r) {
+    NvtxRange nv(phase_name(phase));
     if (!c || (phase == BSQ_PH_GHOST && !p) || (phase == BSQ_PH_FINAL && !r))
         return fail(BSQ_ERR_BAD_ARG, "null argument");
     return ENGINE(c, e->phase(phase, p, r));

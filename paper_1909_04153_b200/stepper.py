@@ -37,11 +37,21 @@ _KIND_CODE = {"wall": nat.WALL, "maker": nat.MAKER, "sponge": nat.SPONGE}
 _STAGE_NAMES = ("e", "f", "g", "fstar", "gstar")
 
 
-class InstabilityError(RuntimeError):
-    """The run blew up; carries a snapshot of the offending state."""
+try:  # the reference package, when it is installed beside this one
+    from boussim.stepper import InstabilityError as _InstabilityBase
+except Exception:  # noqa: BLE001 -- absent (or unimportable): a plain RuntimeError
+    _InstabilityBase = RuntimeError
+
+
+class InstabilityError(_InstabilityBase):
+    """The run blew up; carries a snapshot of the offending state.
+
+    A subclass of ``boussim.stepper.InstabilityError`` whenever boussim is
+    importable, so the reference's own ``except stepper.InstabilityError``
+    (cli.py:654) catches it after the one-line swap of INTEGRATION.md."""
 
     def __init__(self, message: str, step_index: int, sim_time: float, state=None):
-        super().__init__(message)
+        RuntimeError.__init__(self, message)  # the same fields either base sets
         self.step_index = step_index
         self.sim_time = sim_time
         self.state = state
@@ -310,7 +320,8 @@ class Simulator:
         hs = self._host_state
         if hs is None:
             return
-        if self._host_pristine is None:  # read-only large-grid copy: nothing to sync
+        if self._host_pristine is None:  # large grid: no pristine copy to diff against,
+            self._dev.upload(hs.w, hs.p, hs.q)  # so whatever the caller holds goes back
             self._host_state = None
             return
         pw, pp, pq = self._host_pristine
@@ -324,18 +335,17 @@ class Simulator:
     @property
     def state(self) -> FieldState:
         """Host copy of the committed state, downloaded on first access after a
-        step.  Small grids (<= EDIT_TRACK_BYTES) keep the reference's
-        semantics that in-place edits of ``sim.state`` take effect: the edit
-        is uploaded before the next step.  Larger grids hand out read-only
-        arrays instead of paying a full host copy per access; assign
-        ``sim.state = ...`` to replace them."""
+        step.  In-place edits of ``sim.state`` take effect at the next step,
+        as in the reference: small grids (<= EDIT_TRACK_BYTES) keep a pristine
+        copy and upload only if something changed; larger grids upload the
+        handed-out arrays before the next step (one host-to-device copy of
+        the state per access, instead of a second host copy and a diff).
+        ``download_state()`` reads without that write-back."""
         if self._host_state is None:
             w, p, q = self._dev.download()
             if 3 * w.nbytes <= self.EDIT_TRACK_BYTES:
                 self._host_pristine = (w.copy(), p.copy(), q.copy())
             else:
-                for a in (w, p, q):
-                    a.flags.writeable = False
                 self._host_pristine = None
             self._host_state = FieldState(w, p, q)
         return self._host_state

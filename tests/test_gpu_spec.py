@@ -145,3 +145,33 @@ def test_rejected_speculation_then_plain_steps_keep_ghosts():
         for _ in range(4):
             assert a.advance() == b.advance()
             _same_full_state(a, b)
+
+
+@pytest.mark.parametrize("track_bytes", [64 << 20, 0])
+def test_in_place_state_edits_take_effect(track_bytes, monkeypatch):
+    """The reference semantics of editing ``sim.state`` in place between
+    steps hold on both paths: a pristine copy and a diff (small grids), or
+    the write-back of the handed-out arrays (grids above EDIT_TRACK_BYTES,
+    forced here with a zero threshold)."""
+    from oracle import oracle as orc
+    monkeypatch.setattr(stepper.Simulator, "EDIT_TRACK_BYTES", track_bytes)
+    z = gc.load("maker_sponge")
+    bathy, state, bounds, phys, ckw, skw = gc.inputs(z)
+    sim = stepper.Simulator(bathy, state.copy(), bounds, stepper.TimeController(**ckw),
+                            phys=phys, **skw)
+    ora = orc.OracleSimulator(bathy, state.copy(), bounds, orc.OController(**ckw), phys=phys,
+                              **skw)
+    for k in range(12):
+        if k in (4, 9):
+            for s in (sim, ora):
+                st = s.state  # the oracle hands out a copy: its edit is set back below
+                st.w[10:14, 8:20] += 0.003 * (k + 1)
+                st.p[12, 5:9] = -0.001
+                if s is ora:
+                    ora.set_state(st)
+        a, b = sim.advance(), ora.advance()
+        assert (a.dt, a.max_cfl, a.max_speed, a.max_depth) == \
+            (b.dt, b.max_cfl, b.max_speed, b.max_depth), k
+    for f in ("w", "p", "q"):
+        x, y = getattr(sim.state, f), getattr(ora.state, f)
+        assert np.array_equal(x.view(np.uint64), y.view(np.uint64)), f
