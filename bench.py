@@ -238,6 +238,16 @@ def config_line(name, dev, hbm, no_cpu=False):
     return out
 
 
+def physical_cores():
+    """Physical cores of the host (context for cpu_baseline.cores, which is
+    the thread count actually used)."""
+    try:
+        import psutil
+        return psutil.cpu_count(logical=False)
+    except Exception:
+        return None
+
+
 def cpu_threads() -> int:
     """Host threads the CPU legs use: the logical CPUs this process may run on."""
     try:
@@ -299,6 +309,7 @@ def _run_reference(args):
         "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": v, "unit": "Gcell-updates/s", "cores": threads, "kind": "port",
+                         "physical_cores": physical_cores(),
                          "sample": f"{args.steps} full 4096x4096 steps of the per-GPU workload on "
                                    "the C oracle (OpenMP; bitwise = reference)"},
         "e2e": {"value": v, "unit": "Gcell-updates/s", "h2d_bytes_per_step": 0,
@@ -501,6 +512,7 @@ def main():
         threads = cpu_threads()
         v_cpu, wall = cpu_baseline(case, args.cpu_steps, threads)
         cpu = {"value": v_cpu, "unit": "Gcell-updates/s", "cores": threads, "kind": "port",
+               "physical_cores": physical_cores(),
                "sample": f"{args.cpu_steps} full {case.bathy.grid.nx}x{case.bathy.grid.ny} steps "
                          f"(after 1 warm-up) of the same case on the C oracle, {wall:.1f} s"}
 

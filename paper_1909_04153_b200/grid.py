@@ -5,7 +5,8 @@ Same public names and semantics as the reference data model
 (/root/reference/pkg/src/boussim/grid.py:19-194) so a caller's setup code
 ports unchanged; the derived static fields are computed with the same
 numpy expressions, so they are bitwise identical to the reference's
-(pinned by tests/test_host_model.py against tests/golden/).
+(pinned by tests/test_abi_host.py::test_build_bathymetry_bitwise against
+tests/golden/).
 
 Layout: every field is float64, row-major ``[j, i]`` (j north, i east),
 padded with a ``GHOST``-wide frame: shape ``(ny + 4, nx + 4)``.

@@ -22,7 +22,6 @@ from __future__ import annotations
 
 import math
 import os
-import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -128,32 +127,6 @@ def record_gauges(state, recorder: GaugeRecorder, t: float) -> int:
     return recorder.record(state, t)
 
 
-@dataclass(frozen=True)
-class WindowStats:
-    mwl: float
-    u_avg: float
-    v_avg: float
-    hs: float
-    n_samples: int
-
-
-def time_averages(samples: np.ndarray, window: tuple[float, float]) -> WindowStats:
-    """Mean water level, mean velocities and 4-sigma wave height over the
-    samples with t in ``window`` (inclusive) (scenario.py:236-262)."""
-    t0, t1 = window
-    arr = np.asarray(samples, dtype=float).reshape(-1, 6)
-    sel = arr[(arr[:, 0] >= t0) & (arr[:, 0] <= t1)]
-    n = sel.shape[0]
-    if n == 0:
-        raise ValueError(f"no samples in averaging window [{t0}, {t1}]")
-    if n < 100:
-        warnings.warn(f"averaging window holds only {n} samples; statistics will be noisy",
-                      stacklevel=2)
-    eta = sel[:, 1]
-    return WindowStats(mwl=float(eta.mean()), u_avg=float(sel[:, 4].mean()),
-                       v_avg=float(sel[:, 5].mean()), hs=float(4.0 * eta.std()), n_samples=n)
-
-
 class MaxSurfaceTracker:
     """Per-cell running maximum of the interior water surface
     (scenario.py:289-299).
@@ -199,4 +172,4 @@ class MaxSurfaceTracker:
 
 
 __all__ = ["GAUGE_CSV_HEADER", "GaugeSpec", "gauge_cell", "GaugeRecorder", "record_gauges",
-           "WindowStats", "time_averages", "MaxSurfaceTracker", "FieldState"]
+           "MaxSurfaceTracker", "FieldState"]

@@ -116,18 +116,6 @@ def test_dt_history_and_gauge_csv_bytes(tmp_path):
         assert (tmp_path / f"gauge_{g}.csv").read_bytes() == _bytes(z, f"gauge_{g}.csv"), g
 
 
-def test_time_averages():
-    z = _fixture()
-    s = z["series_g_west"]
-    with pytest.warns(UserWarning):
-        st = obs.time_averages(s, (0.0, 0.5))
-    sel = s[(s[:, 0] >= 0.0) & (s[:, 0] <= 0.5)]
-    assert st.n_samples == sel.shape[0] and st.mwl == float(sel[:, 1].mean())
-    assert st.hs == float(4.0 * sel[:, 1].std())
-    with pytest.raises(ValueError):
-        obs.time_averages(s, (100.0, 200.0))
-
-
 # ---------------------------------------------------------------------------- GPU
 
 
