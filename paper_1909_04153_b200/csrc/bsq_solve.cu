@@ -24,6 +24,7 @@
 // clipped on store by the TMA unit.  The forward sweep's dw is stored into
 // the output array and read back by the backward sweep, which overwrites it.
 #include <cstdint>
+#include <cstdio>
 
 #include "bsq_device.cuh"
 #include "bsq_launch.h"
@@ -61,6 +62,15 @@ struct TileGeom {
     static constexpr int SMEM_B = 1024 + RING_B + 2 * TILE_B + 8 * (2 * NS + 2 * NS2);
 };
 
+// An opaque use of all EK fp32 values: instructions that read them cannot
+// move above the point where every one of them is computed.
+__device__ __forceinline__ void rcp_fence(float (&v)[32]) {
+#pragma unroll
+    for (int k = 0; k < 32; k += 8)
+        asm volatile("" : "+f"(v[k]), "+f"(v[k + 1]), "+f"(v[k + 2]), "+f"(v[k + 3]),
+                     "+f"(v[k + 4]), "+f"(v[k + 5]), "+f"(v[k + 6]), "+f"(v[k + 7]));
+}
+
 // element offset of (line ln, chunk element k) inside a tile
 template <class T, bool XDIR>
 __device__ __forceinline__ int toff(int ln, int k) {
@@ -82,7 +92,7 @@ __device__ __forceinline__ int toff(int ln, int k) {
 // instead of 4; 0.347 -> 0.310 ms per solve at 4096^2) whenever every pivot's
 // exponent is within +-1000 (PIV_RDEN_INRANGE, checked at factor time)
 template <class T, bool XDIR, bool POS, bool RDEN_ONCHIP, bool EXD>
-__device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
+__device__ __forceinline__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
                                 int line0, unsigned char *smem, int mode) {
     using G = TileGeom<T, RDEN_ONCHIP>;
     constexpr int EK = G::EK, TILE = G::TILE, NS = G::NS, NS2 = G::NS2, FT = G::FT;
@@ -119,6 +129,9 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
     __syncthreads();
 
     // ---- forward sweep --------------------------------------------------------
+#ifdef BSQ_SOLVE_CLOCKS
+    const long long t_start = clock64();
+#endif
     constexpr int SUB = G::SUB, SUBT = G::SUBT;
     const int nsc = (nc + SUB - 1) / SUB;  // ring stages (super-chunks) per sweep
     if (mode == SOLVE_YBWD) {
@@ -193,6 +206,11 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
                 if (RDEN_ONCHIP) {
 #pragma unroll
                     for (int k = 0; k < EK; k++) nv[k] = -rcp_rn_inrange(dv[k]);
+                    // fp32: the chunk's reciprocals complete before its
+                    // recurrence starts (interleaved element by element, each
+                    // step waited on the next element's MUFU + Newton chain);
+                    // fp64 measured no difference either way
+                    if constexpr (sizeof(T) == 4) rcp_fence(nv);
                 }
 #pragma unroll
                 for (int k = 0; k < EK; k++) {
@@ -304,6 +322,10 @@ __device__ void solve_lines_tma(const Consts<T> &C, const SolveMaps &M, const So
         }
         if (sint && lv) S.x_out[line] = xv;  // the south rank continues from here
         if (lane == 0) bulk_wait_all();
+#ifdef BSQ_SOLVE_CLOCKS
+        if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+            printf("solve cta %d n %d total %lld cycles\n", (int)blockIdx.x, n, clock64() - t_start);
+#endif
     }
 }
 
@@ -312,8 +334,16 @@ template <class T, bool POS, bool ONCHIP, bool EXD>
 __global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_constant__ SolveMaps M,
                                                   SolvePtrs<T> S, int nbx, int mode) {
     extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-B alignment of the ring.  fp32: pointer arithmetic on the shared
+    // array keeps the address space (LDS/STS with 32-bit addresses; with the
+    // reciprocal batch below, fp32 solve 0.1685 -> 0.149 ms).  fp64 keeps the
+    // generic form: its schedule with LDS/STS measured slower (0.307 -> 0.320).
+    unsigned char *smem;
+    if constexpr (sizeof(T) == 4)
+        smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    else
+        smem = reinterpret_cast<unsigned char *>(
+            (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     pdl_trigger();
     pdl_wait();
     if ((int)blockIdx.x < nbx)
