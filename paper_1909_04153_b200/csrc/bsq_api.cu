@@ -665,6 +665,11 @@ struct Engine : EngineBase {
 
     int build_maps() {
         SolveMaps &M = maps;
+        M.xp_rhs = arr[A_US];
+        M.xp_a = arr[A_AX];
+        M.xp_den = arr[A_DENX];
+        M.xp_rden = arr[A_RDENX];
+        M.xp_cw = arr[A_CWX];
         int rc;
         if ((rc = build_stage_maps())) return rc;
         if ((rc = make_map(&M.x_rhs, arr[A_US], true)) || (rc = make_map(&M.x_a, arr[A_AX], true)) ||
@@ -953,6 +958,7 @@ struct Engine : EngineBase {
         const int k = (phase == 2 && scratch) ? 2 : nxt_state;
         maps.x_out = map_xout[k];
         maps.y_out = map_yout[k];
+        maps.xp_out = k == 2 ? arr[A_P2] : Pp(k);
         return maps;
     }
 

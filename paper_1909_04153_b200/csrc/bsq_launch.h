@@ -69,6 +69,10 @@ enum SolveMode { SOLVE_FULL = 0, SOLVE_X_YFWD = 1, SOLVE_YBWD = 2 };
 struct SolveMaps {
     CUtensorMap x_rhs, x_a, x_den, x_rden, x_cw, x_out;
     CUtensorMap y_rhs, y_a, y_den, y_rden, y_cw, y_out;
+    // the x-direction arrays themselves (padded layout), for the warp-per-line
+    // path of few long x lines (bsq_solve.cu solve_xline_warp)
+    const void *xp_rhs, *xp_a, *xp_den, *xp_rden, *xp_cw;
+    void *xp_out;
 };
 
 // solver="cr": the reference's odd-even cyclic reduction (bsq_cr.cu)

@@ -24,6 +24,7 @@
 // clipped on store by the TMA unit.  The forward sweep's dw is stored into
 // the output array and read back by the backward sweep, which overwrites it.
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 
 #include "bsq_device.cuh"
@@ -329,10 +330,139 @@ __device__ __forceinline__ void solve_lines_tma(const Consts<T> &C, const SolveM
     }
 }
 
+// Few long x lines (C1: 5 lines of 1024, C2: 64 of 2048): the TMA ring above
+// is paced by its data path there (without the recurrence it alone takes 80 %
+// of C1's solve), so these lines run one warp per line instead.  The lanes
+// load 32 consecutive elements of the line at a time (coalesced, two chunks
+// ahead), compute the chunk's pivot reciprocals side by side, and stage the
+// operands in shared memory; every lane then runs the same recurrence from
+// broadcast reads (no divergence), lane k keeping element k.  dw stays in
+// shared memory for the whole line (no round trip through HBM), and the back
+// substitution writes the result once.  Same operations and order as
+// thomas_batch with the folded ghosts (_kernels.py:360-381, implicit.py:178-179).
+constexpr int XW_LINES = 2;  // x lines (warps) per CTA on this path
+#ifndef BSQ_XW_MAX_LINES
+#define BSQ_XW_MAX_LINES 256  // at most this many x lines take the path (one wave)
+#endif
+constexpr int XW_MAX_LINES = BSQ_XW_MAX_LINES;
+template <class T>
+__host__ __device__ constexpr int xw_smem_elems(int n) { return n + 5 * 32; }
+
+template <class T, bool POS, bool ONCHIP, bool EXD>
+__device__ __forceinline__ void solve_xline_warp(const Consts<T> &C, const SolveMaps &M,
+                                                 const SolvePtrs<T> &S, int line, T *sm) {
+    const Layout L = C.L;
+    const int n = L.nx, lane = threadIdx.x & 31;
+    if (line >= L.ny) return;
+    const long row = L.at(GL + line, GL);
+    const T *R = reinterpret_cast<const T *>(M.xp_rhs) + row;
+    const T *A = reinterpret_cast<const T *>(M.xp_a) + row;
+    const T *D = reinterpret_cast<const T *>(M.xp_den) + row;
+    const T *RD = reinterpret_cast<const T *>(M.xp_rden) + row;
+    const T *CW = reinterpret_cast<const T *>(M.xp_cw) + row;
+    T *OUT = reinterpret_cast<T *>(M.xp_out) + row;
+    T *dws = sm, *sr = sm + n, *sa = sr + 32, *sd = sa + 32, *sn = sd + 32, *sc = sn + 32;
+    const T g0 = S.gp[L.at(GL + line, GL - 1)];
+    const T g1 = S.gp[L.at(GL + line, n + GL)];
+    const T cl = S.cx_last[line];
+    auto step = [&](T num, T den, T nr) -> T {
+        if (EXD) return num / den;
+        return POS ? div_static_pos(num, den, nr) : div_static(num, den, -nr);
+    };
+    const int nc = (n + 31) / 32;
+    // ---- forward sweep: dw_e = (r_e - a_e dw_{e-1}) / den_e, dw_{-1} = g0
+    T fr[2], fa[2], fd[2], fn[2];  // operands of chunks c+1, c+2 for this lane
+    auto fetch = [&](int c, int k) {
+        const int e = c * 32 + lane;
+        const bool in = e < n;
+        fr[k] = in ? R[e] : T(0);
+        fa[k] = in ? A[e] : T(0);
+        fd[k] = in ? D[e] : T(1);
+        fn[k] = (in && !ONCHIP) ? RD[e] : T(0);
+    };
+    T r0, a0, d0, n0;
+    {
+        fetch(0, 0);
+        r0 = fr[0], a0 = fa[0], d0 = fd[0], n0 = fn[0];
+        if (nc > 1) fetch(1, 0);
+        if (nc > 2) fetch(2, 1);
+    }
+    T dw = g0;
+    for (int c = 0; c < nc; c++) {
+        const T nr0 = ONCHIP ? -rcp_rn_inrange(d0) : n0;
+        sr[lane] = r0, sa[lane] = a0, sd[lane] = d0, sn[lane] = nr0;
+        __syncwarp();
+        // rotate the prefetch window and request chunk c+3
+        r0 = fr[0], a0 = fa[0], d0 = fd[0], n0 = fn[0];
+        fr[0] = fr[1], fa[0] = fa[1], fd[0] = fd[1], fn[0] = fn[1];
+        if (c + 3 < nc) fetch(c + 3, 1);
+        const int e0 = c * 32, kmax = min(32, n - e0);
+        T mine = T(0);
+        if (e0 > 0 && kmax == 32 && e0 + 32 < n) {  // interior chunk
+#pragma unroll
+            for (int k = 0; k < 32; k++) {
+                dw = step(sr[k] - sa[k] * dw, sd[k], sn[k]);
+                mine = lane == k ? dw : mine;
+            }
+        } else {
+            for (int k = 0; k < kmax; k++) {
+                const int e = e0 + k;
+                T num;
+                if (e == n - 1 && n > 1) num = (sr[k] - cl * g1) - sa[k] * dw;  // far ghost first
+                else num = sr[k] - sa[k] * dw;                                 // e = 0: a_0 g0
+                if (e == n - 1 && n == 1) num = num - cl * g1;
+                dw = step(num, sd[k], sn[k]);
+                mine = lane == k ? dw : mine;
+            }
+        }
+        if (lane < kmax) dws[e0 + lane] = mine;
+        __syncwarp();
+    }
+    // ---- back substitution: x_{n-1} = dw_{n-1}, x_e = dw_e - cw_e x_{e+1}
+    T fc[2];
+    auto fetchc = [&](int c, int k) {
+        const int e = c * 32 + lane;
+        fc[k] = e < n ? CW[e] : T(0);
+    };
+    T c0v;
+    {
+        fetchc(nc - 1, 0);
+        c0v = fc[0];
+        if (nc > 1) fetchc(nc - 2, 0);
+        if (nc > 2) fetchc(nc - 3, 1);
+    }
+    T xv = T(0);
+    for (int c = nc - 1; c >= 0; c--) {
+        sc[lane] = c0v;
+        __syncwarp();
+        c0v = fc[0];
+        fc[0] = fc[1];
+        if (c - 3 >= 0) fetchc(c - 3, 1);
+        const int e0 = c * 32, kmax = min(32, n - e0);
+        T mine = T(0);
+        if (kmax == 32 && e0 + 32 < n) {
+#pragma unroll
+            for (int k = 31; k >= 0; k--) {
+                xv = dws[e0 + k] - sc[k] * xv;
+                mine = lane == k ? xv : mine;
+            }
+        } else {
+            for (int k = kmax - 1; k >= 0; k--) {
+                const int e = e0 + k;
+                xv = e == n - 1 ? dws[e] : dws[e] - sc[k] * xv;
+                mine = lane == k ? xv : mine;
+            }
+        }
+        if (lane < kmax) OUT[e0 + lane] = mine;
+        __syncwarp();
+    }
+}
+
 // Blocks [0, nbx) take x lines (rows -> P); blocks [nbx, ...) y lines (columns -> Q).
+// xwarp: the x-line blocks run solve_xline_warp, XW_LINES lines each.
 template <class T, bool POS, bool ONCHIP, bool EXD>
 __global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_constant__ SolveMaps M,
-                                                  SolvePtrs<T> S, int nbx, int mode) {
+                                                  SolvePtrs<T> S, int nbx, int mode, int xwarp) {
     extern __shared__ unsigned char smem_raw[];
     // 1024-B alignment of the ring.  fp32: pointer arithmetic on the shared
     // array keeps the address space (LDS/STS with 32-bit addresses; with the
@@ -346,7 +476,12 @@ __global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_cons
             (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     pdl_trigger();
     pdl_wait();
-    if ((int)blockIdx.x < nbx)
+    if ((int)blockIdx.x < nbx && xwarp) {
+        // straight from the shared array (no alignment round trip): LDS/STS
+        const int w = threadIdx.x >> 5;
+        T *sm = reinterpret_cast<T *>(smem_raw) + w * xw_smem_elems<T>(C.L.nx);
+        solve_xline_warp<T, POS, ONCHIP, EXD>(C, M, S, blockIdx.x * XW_LINES + w, sm);
+    } else if ((int)blockIdx.x < nbx)
         solve_lines_tma<T, true, POS, ONCHIP, EXD>(C, M, S, blockIdx.x * NLINE, smem, mode);
     else
         solve_lines_tma<T, false, POS, ONCHIP, EXD>(C, M, S, (blockIdx.x - nbx) * NLINE, smem, mode);
@@ -358,8 +493,18 @@ __global__ void __launch_bounds__(64) k_solve_tma(Consts<T> C, const __grid_cons
 template <class T>
 void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S, int pivots,
                   cudaStream_t st, int mode) {
-    const int nbx = (C.L.ny + NLINE - 1) / NLINE, nby = (C.L.nx + NLINE - 1) / NLINE;
+    // few long x lines: the warp-per-line path (one wave of CTAs, the whole
+    // line's dw in shared memory)
     const int smem_on = TileGeom<T, true>::SMEM_B, smem_off = TileGeom<T, false>::SMEM_B;
+    const size_t xw_smem = 1024 + sizeof(T) * XW_LINES * (size_t)xw_smem_elems<T>(C.L.nx);
+    static const int xw_env = [] {
+        const char *e = std::getenv("BSQ_SOLVE_XWARP");  // A/B: 0 off, 1 forced
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    const bool xwarp = mode != SOLVE_YBWD && xw_smem <= (size_t)smem_on &&
+                       (xw_env == 1 || (xw_env < 0 && C.L.ny <= XW_MAX_LINES));
+    const int nbx = xwarp ? (C.L.ny + XW_LINES - 1) / XW_LINES : (C.L.ny + NLINE - 1) / NLINE;
+    const int nby = (C.L.nx + NLINE - 1) / NLINE;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(k_solve_tma<T, true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_on);
@@ -378,15 +523,15 @@ void launch_solve(const Consts<T> &C, const SolveMaps &M, const SolvePtrs<T> &S,
 #endif
     dim3 g(bx + nby), b(64);
     if (S.exact)
-        launch_k(k_solve_tma<T, false, false, true>, g, b, smem_off, st, C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, false, false, true>, g, b, smem_off, st, C, M, S, bx, mode, (int)xwarp);
     else if (pos && onchip)
-        launch_k(k_solve_tma<T, true, true, false>, g, b, smem_on, st, C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, true, true, false>, g, b, smem_on, st, C, M, S, bx, mode, (int)xwarp);
     else if (pos)
-        launch_k(k_solve_tma<T, true, false, false>, g, b, smem_off, st, C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, true, false, false>, g, b, smem_off, st, C, M, S, bx, mode, (int)xwarp);
     else if (onchip)
-        launch_k(k_solve_tma<T, false, true, false>, g, b, smem_on, st, C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, false, true, false>, g, b, smem_on, st, C, M, S, bx, mode, (int)xwarp);
     else
-        launch_k(k_solve_tma<T, false, false, false>, g, b, smem_off, st, C, M, S, bx, mode);
+        launch_k(k_solve_tma<T, false, false, false>, g, b, smem_off, st, C, M, S, bx, mode, (int)xwarp);
 }
 
 #if BSQ_INST_F64
