@@ -34,6 +34,11 @@ constexpr int FT = FX * FY, FWARPS = FT / 32;
 #ifndef BSQ_FINAL_MINB
 #define BSQ_FINAL_MINB 3  // 80 registers, no spills (4: 64 with spills, 0.148 vs 0.133 ms)
 #endif
+#ifndef BSQ_FINAL_MINB32
+#define BSQ_FINAL_MINB32 4  // fp32: 63 registers without spills (0.0982 -> 0.0971 ms)
+#endif
+template <class T>
+constexpr int final_minb() { return sizeof(T) == 8 ? BSQ_FINAL_MINB : BSQ_FINAL_MINB32; }
 
 struct Red {
     double rate, speed, depth, dev, clamp;
@@ -258,7 +263,7 @@ static __device__ void spec_next(const DevParams &P, double max_rate, DevParams 
 // partial and counter per CTA instead of per tile: the per-tile barrier and
 // atomic were the kernel's top stall after the loads).
 template <class T, bool SPIKE, bool FAST, bool EXT>
-__global__ void __launch_bounds__(FT, BSQ_FINAL_MINB) k_final(Consts<T> C, FinalPtrs<T> F,
+__global__ void __launch_bounds__(FT, final_minb<T>()) k_final(Consts<T> C, FinalPtrs<T> F,
                                                               int tiles_x, int ntiles) {
     __shared__ bool am_last;
     pdl_trigger();
