@@ -347,14 +347,23 @@ def main():
     from paper_1909_04153_b200.scenario import make_case
 
     dist = comm = None
+    # BSQ_DIST_BACKEND=gloo: ranks exchange through host memory and may share a
+    # GPU (the functional multi-rank test on a one-GPU box); timing is then
+    # not a multi-GPU measurement.  NCCL (one GPU per rank) is the product.
+    backend = os.environ.get("BSQ_DIST_BACKEND", "nccl")
     if world > 1:
         import torch.distributed as dist_mod
         from paper_1909_04153_b200.parallel import DistComm, ShardedSimulator
         dist = dist_mod
-        torch.cuda.set_device(local)
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator set-up (nranks) in the log
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator set-up (nranks) in the log
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend)
         dist.barrier()  # communicator up on every rank before the first P2P exchange
         comm = DistComm()
     dev = torch.device("cuda", local if world > 1 else 0)
@@ -388,7 +397,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

@@ -20,7 +20,7 @@
 namespace bsq {
 
 #ifndef BSQ_CR_THREADS
-#define BSQ_CR_THREADS 512
+#define BSQ_CR_THREADS 1024  // 512: 1.46, 256: 1.83, 1024: 1.42 ms per 4096^2 solve
 #endif
 constexpr int CR_THREADS = BSQ_CR_THREADS;
 

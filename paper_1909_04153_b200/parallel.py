@@ -176,6 +176,19 @@ class DistComm:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.local = [self.rank]
+        # a non-NCCL backend (gloo: the CPU tests, and ranks sharing one GPU in
+        # the functional multi-process GPU test) moves device rows through
+        # host memory; NCCL sends device memory directly
+        self.staged = dist.get_backend(group) != "nccl"
+
+    def _wire(self, t):
+        """What goes on the wire for tensor ``t`` (a host copy when staged)."""
+        return t.cpu() if (self.staged and t.is_cuda) else t
+
+    def _landing(self, t):
+        """An empty buffer the transport can receive ``t``'s shape into."""
+        return torch.empty(t.shape, dtype=t.dtype, device="cpu") if (self.staged and t.is_cuda) \
+            else torch.empty_like(t)
 
     def _dev(self):
         return torch.device("cuda", torch.cuda.current_device()) \
@@ -214,17 +227,25 @@ class DistComm:
         queue ``inner()`` on the current stream while they are in flight, then
         make the current stream wait for them."""
         d, r, ops = self.dist, self.rank, []
+        wire = []  # (staged landing buffer, device destination)
         if send_up is not None:
-            ops.append(d.P2POp(d.isend, send_up, r + 1, group=self.group))
-            ops.append(d.P2POp(d.irecv, recv_up, r + 1, group=self.group))
+            land = self._landing(recv_up)
+            wire.append((land, recv_up))
+            ops.append(d.P2POp(d.isend, self._wire(send_up), r + 1, group=self.group))
+            ops.append(d.P2POp(d.irecv, land, r + 1, group=self.group))
         if send_dn is not None:
-            ops.append(d.P2POp(d.isend, send_dn, r - 1, group=self.group))
-            ops.append(d.P2POp(d.irecv, recv_dn, r - 1, group=self.group))
+            land = self._landing(recv_dn)
+            wire.append((land, recv_dn))
+            ops.append(d.P2POp(d.isend, self._wire(send_dn), r - 1, group=self.group))
+            ops.append(d.P2POp(d.irecv, land, r - 1, group=self.group))
         works = d.batch_isend_irecv(ops) if ops else []
         if inner is not None:
             inner()  # interior rows: overlap the transfers
         for w in works:
             w.wait()
+        for land, dst in wire:
+            if land is not dst:
+                dst.copy_(land)
 
     def halo(self, strips, ids, nrows: int, stream, inner=None):
         s = strips[self.rank]
@@ -243,18 +264,24 @@ class DistComm:
                 if dn:
                     v[GHOST - nrows:GHOST].copy_(recv_dn[k * nrows:(k + 1) * nrows])
 
+    def _recv_into(self, dst, src_rank):
+        land = self._landing(dst)
+        self.dist.recv(land, src_rank, group=self.group)
+        if land is not dst:
+            dst.copy_(land)
+
     def pipeline(self, strips, ph_f: int, ph_b: int, stream):
         d, r, s = self.dist, self.rank, strips[self.rank]
         with torch.cuda.stream(stream):
             if r > 0:
-                d.recv(s.vector(nat.ARR_DW_IN), r - 1, group=self.group)
+                self._recv_into(s.vector(nat.ARR_DW_IN), r - 1)
             s.phase(ph_f)
             if r + 1 < self.world:
-                d.send(s.vector(nat.ARR_DW_OUT), r + 1, group=self.group)
-                d.recv(s.vector(nat.ARR_X_IN), r + 1, group=self.group)
+                d.send(self._wire(s.vector(nat.ARR_DW_OUT)), r + 1, group=self.group)
+                self._recv_into(s.vector(nat.ARR_X_IN), r + 1)
             s.phase(ph_b)
             if r > 0:
-                d.send(s.vector(nat.ARR_X_OUT), r - 1, group=self.group)
+                d.send(self._wire(s.vector(nat.ARR_X_OUT)), r - 1, group=self.group)
 
     def reduce(self, parts: list, nx: int, rows0: list):
         """One all_gather per step: every rank's reductions (maxima, NaN flag as
@@ -339,9 +366,10 @@ class DistComm:
         with torch.cuda.stream(stream):
             R, n = s.rows(arr), s.ny
             mine = torch.stack([R[GHOST, GHOST:-GHOST], R[GHOST + n - 1, GHOST:-GHOST]]).contiguous()
-            bufs = [torch.empty_like(mine) for _ in range(self.world)]
-            self.dist.all_gather(bufs, mine, group=self.group)
-            yb = torch.stack(bufs).contiguous()
+            wire = self._wire(mine)
+            bufs = [torch.empty_like(wire) for _ in range(self.world)]
+            self.dist.all_gather(bufs, wire, group=self.group)
+            yb = torch.stack(bufs).to(mine.device).contiguous()
         return {self.rank: yb}
 
 
