@@ -66,8 +66,22 @@ __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which,
     const long nframe = 4L * nxt + 4L * ny;
     // the frame save: every frame cell is written by exactly one thread, which
     // reads its old value first
-    auto keep = [&](int f, int J, int I) {
-        if (save) save[f * nframe + frame_index(nx, ny, J, I)] = dst[f][C.L.at(J, I)];
+    // every read of a thread (its sources, and the old ghost values the frame
+    // save keeps) is issued before its first store: the compiler cannot reorder
+    // them itself (src and dst may be the same arrays), and serialized they
+    // made the fill three memory round trips long
+    auto write3 = [&](int J, int I, const T (&v)[3]) {
+        const long o = C.L.at(J, I);
+        if (save) {
+            T old[3];
+#pragma unroll
+            for (int f = 0; f < 3; f++) old[f] = dst[f][o];
+            const long fi = frame_index(nx, ny, J, I);
+#pragma unroll
+            for (int f = 0; f < 3; f++) save[f * nframe + fi] = old[f];
+        }
+#pragma unroll
+        for (int f = 0; f < 3; f++) dst[f][o] = v[f];
     };
     if (k < 4 * nyt) {
         int J = k >> 2;
@@ -80,20 +94,18 @@ __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which,
         if (C.side_kind[side] == KIND_MAKER) {
             double gw = which ? P->gw_n[side] : P->gw_t[side];
             double gf = which ? P->gf_n[side] : P->gf_t[side];
-            for (int f = 0; f < 3; f++) keep(f, J, I);
-            dst_w[C.L.at(J, I)] = T(gw);
-            dst_p[C.L.at(J, I)] = side == SIDE_W ? T(gf) : T(-gf);
-            dst_q[C.L.at(J, I)] = T(0);
+            const T v[3] = {T(gw), side == SIDE_W ? T(gf) : T(-gf), T(0)};
+            write3(J, I, v);
             return;
         }
         int Im = side == SIDE_W ? (I == GL - 1 ? GL : GL + 1) : (I == nxt - GL ? nxt - GL - 1 : nxt - GL - 2);
+        T v[3];
 #pragma unroll
         for (int f = 0; f < 3; f++) {
             T cur = interior_row ? src[f][C.L.at(J, Im)] : ns_value(C, P, which, f, J, Im, src[f]);
-            T s = f == 1 ? T(-1) : T(1);  // P is the wall-normal flux on E/W
-            keep(f, J, I);
-            dst[f][C.L.at(J, I)] = s * cur;
+            v[f] = (f == 1 ? T(-1) : T(1)) * cur;  // P is the wall-normal flux on E/W
         }
+        write3(J, I, v);
         return;
     }
     k -= 4 * nyt;
@@ -102,11 +114,10 @@ __global__ void k_ghost(Consts<T> C, const DevParams *__restrict__ P, int which,
         int r = k & 3;
         int J = r < 2 ? r : nyt - 4 + r;
         if (C.side_kind[J < GL ? SIDE_S : SIDE_N] == KIND_INTERNAL) return;
+        T v[3];
 #pragma unroll
-        for (int f = 0; f < 3; f++) {
-            keep(f, J, I);
-            dst[f][C.L.at(J, I)] = ns_value(C, P, which, f, J, I, src[f]);
-        }
+        for (int f = 0; f < 3; f++) v[f] = ns_value(C, P, which, f, J, I, src[f]);
+        write3(J, I, v);
     }
 }
 
