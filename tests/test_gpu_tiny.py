@@ -125,3 +125,17 @@ def test_tiny_momenta_on_y_strips_bitwise():
     for f in ("w", "p", "q"):
         got, want = getattr(sim.state, f), getattr(ora.state, f)
         assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), f
+
+
+@pytest.mark.parametrize("nx,ny", [(4099, 5), (5000, 6), (1500, 257)])
+def test_long_x_lines_paths_bitwise(nx, ny):
+    """Few long x lines: the warp-per-line solve up to the shared-memory limit
+    (4099 cells: the line's dw on chip), the TMA ring beyond it (5000 cells)
+    and above the line-count threshold (257 lines) -- all bitwise vs the
+    oracle, ghosts folded at both ends of every line."""
+    grid = Grid(nx, ny, 0.05, 0.05)
+    xc, _ = np.meshgrid(grid.x_centers(), grid.y_centers())
+    bathy = build_bathymetry(grid, -0.3 - 0.05 * np.sin(0.01 * xc), ws=0.0)
+    st = still_state(bathy)
+    st.w += 0.01 * np.exp(-((np.pad(xc, 2, mode="edge") - 0.3 * nx * 0.05) ** 2) / 4.0)
+    run_both(bathy, st, walls(), 6, dt_init=0.004)
