@@ -186,9 +186,10 @@ class DistComm:
         return t.cpu() if (self.staged and t.is_cuda) else t
 
     def _landing(self, t):
-        """An empty buffer the transport can receive ``t``'s shape into."""
+        """Where the transport receives into for destination ``t``: ``t``
+        itself, or a host buffer copied into it afterwards when staged."""
         return torch.empty(t.shape, dtype=t.dtype, device="cpu") if (self.staged and t.is_cuda) \
-            else torch.empty_like(t)
+            else t
 
     def _dev(self):
         return torch.device("cuda", torch.cuda.current_device()) \
