@@ -78,7 +78,8 @@ enum Arr {
     A_BE, A_DEP, A_DDX, A_DDY, A_BFX, A_BFY,
     A_AX, A_DENX, A_RDENX, A_CWX, A_AY, A_DENY, A_RDENY, A_CWY,
     A_BU, A_BV, A_US, A_VS, A_P2, A_Q2,
-    A_BX, A_CX, A_BY, A_CY,  // diagonals for solver="cr"
+    A_BX, A_CX, A_BY, A_CY,  // diagonals for solver="cr" (y ones transposed: [column][row])
+    A_AYT,                   // solver="cr": the y sub-diagonal transposed
     A_SPV, A_SPW,            // BSQ_Y_SPIKE: south / north coupling spikes
     A_W2,                    // third w buffer: the speculative next stage writes here
     A_HIST0,  // 4 slots x 5 fields follow
@@ -94,7 +95,7 @@ bool spike_mode(const bsq_desc *d) {
 
 // arrays a context does not use take no memory
 bool array_used(const bsq_desc *d, int k) {
-    if (k >= A_BX && k <= A_CY) return d->solver == BSQ_CR;
+    if (k >= A_BX && k <= A_AYT) return d->solver == BSQ_CR;
     if (k == A_SPV || k == A_SPW) return spike_mode(d);
     return true;
 }
@@ -426,6 +427,10 @@ struct Engine : EngineBase {
         const long E = L.elems();
         std::vector<T> ax(E, T(0)), denx(E, T(1)), rdenx(E, T(-1)), cwx(E, T(0));
         std::vector<T> bxv(E, T(1)), cxv(E, T(0)), byv(E, T(1)), cyv(E, T(0));  // for "cr"
+        // "cr" y lines read their diagonals contiguously: column i's element j
+        // at i * ny + j (the right-hand side and the result stay in the
+        // padded layout)
+        std::vector<T> ayt(d.solver == BSQ_CR ? E : 0, T(0));
         std::vector<T> ay(E, T(0)), deny(E, T(1)), rdeny(E, T(-1)), cwy(E, T(0));
         std::vector<T> cxl(ny), cyl(nx);
         const double six_dx = 6.0 * d.dx, six_dy = 6.0 * d.dy;
@@ -474,8 +479,12 @@ struct Engine : EngineBase {
                 const double den = (j == 0 && !cont) ? b : b - a * cw_prev;
                 const double cw = cc / den;
                 put(ay, deny, rdeny, cwy, L.at(j + GL, i + GL), a, den, cw);
-                byv[L.at(j + GL, i + GL)] = T(b);
-                cyv[L.at(j + GL, i + GL)] = T(cc);
+                if (d.solver == BSQ_CR) {
+                    const long t = (long)i * ny + j;
+                    ayt[t] = T(a);
+                    byv[t] = T(b);
+                    cyv[t] = T(cc);
+                }
                 cw_prev = cw;
                 if (j == ny - 1) cyl[i] = T(cc);
             }
@@ -486,11 +495,11 @@ struct Engine : EngineBase {
         rden_inrange = inrange;
         if (spike) make_spikes(ay, deny, cwy, cyl);
         const size_t B = sizeof(T) * E;
-        const std::vector<T> *src[12] = {&ax, &denx, &rdenx, &cwx, &ay, &deny, &rdeny, &cwy,
-                                         &bxv, &cxv, &byv, &cyv};
-        const int dst[12] = {A_AX, A_DENX, A_RDENX, A_CWX, A_AY, A_DENY, A_RDENY, A_CWY,
-                             A_BX, A_CX, A_BY, A_CY};
-        for (int k = 0; k < (d.solver == BSQ_CR ? 12 : 8); k++)
+        const std::vector<T> *src[13] = {&ax, &denx, &rdenx, &cwx, &ay, &deny, &rdeny, &cwy,
+                                         &bxv, &cxv, &byv, &cyv, &ayt};
+        const int dst[13] = {A_AX, A_DENX, A_RDENX, A_CWX, A_AY, A_DENY, A_RDENY, A_CWY,
+                             A_BX, A_CX, A_BY, A_CY, A_AYT};
+        for (int k = 0; k < (d.solver == BSQ_CR ? 13 : 8); k++)
             CU(cudaMemcpyAsync(arr[dst[k]], src[k]->data(), B, cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(cx_last, cxl.data(), sizeof(T) * ny, cudaMemcpyHostToDevice, st));
         CU(cudaMemcpyAsync(cy_last, cyl.data(), sizeof(T) * nx, cudaMemcpyHostToDevice, st));
@@ -1296,7 +1305,7 @@ struct Engine : EngineBase {
         K.ax = arr[A_AX];
         K.bx = arr[A_BX];
         K.cx = arr[A_CX];
-        K.ay = arr[A_AY];
+        K.ay = arr[A_AYT];  // transposed, as by / cy
         K.by = arr[A_BY];
         K.cy = arr[A_CY];
         K.rx = arr[A_US];

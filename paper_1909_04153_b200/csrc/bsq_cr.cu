@@ -44,24 +44,27 @@ __device__ void cr_line(const Consts<T> &C, const CrPtrs<T> &K, int line, T *sm,
     const T *Cc = XDIR ? K.cx : K.cy;
     const T *R = XDIR ? K.rx : K.ry;
     auto off = [&](int e) -> long { return XDIR ? L.at(GL + line, GL + e) : L.at(GL + e, GL + line); };
+    // the diagonals: padded layout in x, transposed (contiguous per line) in y
+    auto coff = [&](int e) -> long { return XDIR ? off(e) : (long)line * L.ny + e; };
     // load + ghost folding (implicit.py:178-179 / :190-191), identity padding
 #pragma unroll 4
     for (int i = threadIdx.x; i < n2; i += blockDim.x) {
         if (i < n) {
-            const long o = off(i);
+            const long o = off(i), oc = coff(i);
             T rv = R[o];
+            const T av = A[oc], cv = Cc[oc];
             if (i == 0) {
                 const T g0 = XDIR ? K.gp[L.at(GL + line, GL - 1)] : K.gq[L.at(GL - 1, GL + line)];
-                rv = rv - A[o] * g0;
+                rv = rv - av * g0;
             }
             if (i == n - 1) {
                 const T g1 = XDIR ? K.gp[L.at(GL + line, n + GL)] : K.gq[L.at(n + GL, GL + line)];
-                rv = rv - Cc[o] * g1;
+                rv = rv - cv * g1;
             }
             const int j = crs(i);
-            a[j] = A[o];
-            b[j] = B[o];
-            c[j] = Cc[o];
+            a[j] = av;
+            b[j] = B[oc];
+            c[j] = cv;
             r[j] = rv;
         } else {
             const int j = crs(i);
@@ -157,7 +160,15 @@ void launch_cr(const Consts<T> &C, const CrPtrs<T> &K, cudaStream_t st) {
     const int n2x = pow2_at_least(C.L.nx), n2y = pow2_at_least(C.L.ny);
     const size_t smem = cr_smem_bytes(C.L.nx, C.L.ny, sizeof(T));
     cudaFuncSetAttribute(k_cr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cr<T><<<C.L.ny + C.L.nx, CR_THREADS, smem, st>>>(C, K, C.L.ny, n2x, n2y);
+    // one thread per row of the first reduction level, at most 512 below
+    // 4096-row lines (C1, 1024 rows: 512 threads 0.017 ms per solve, 1024:
+    // 0.033; C2, 2048 rows: 512 0.054, 1024 0.109) and CR_THREADS from there
+    // (4096^2: 512 1.46, 1024 1.42 ms)
+    const int n2 = n2x > n2y ? n2x : n2y;
+    const int cap = n2 >= 4096 ? CR_THREADS : 512;
+    int threads = n2 / 2 < cap ? n2 / 2 : cap;
+    threads = threads < 64 ? 64 : (threads + 31) / 32 * 32;
+    k_cr<T><<<C.L.ny + C.L.nx, threads, smem, st>>>(C, K, C.L.ny, n2x, n2y);
 }
 
 #if BSQ_INST_F64

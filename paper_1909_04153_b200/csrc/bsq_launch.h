@@ -78,7 +78,8 @@ struct SolveMaps {
 // solver="cr": the reference's odd-even cyclic reduction (bsq_cr.cu)
 template <class T>
 struct CrPtrs {
-    const T *ax, *bx, *cx, *ay, *by, *cy;  // the operator's diagonals
+    const T *ax, *bx, *cx, *ay, *by, *cy;  // the operator's diagonals (x: padded layout;
+                                           // y: transposed, column i's row j at i*ny + j)
     const T *rx, *ry;                      // right-hand sides (ghosts folded in-kernel)
     const T *gp, *gq;                      // ghost sources, as SolvePtrs
     T *outx, *outy;
