@@ -15,7 +15,7 @@ from paper_1909_04153_b200 import stepper
 from paper_1909_04153_b200.grid import Grid, PhysParams, build_bathymetry, still_state
 
 pytestmark = pytest.mark.gpu
-SEEDS = list(range(40))
+SEEDS = list(range(int(__import__("os").environ.get("BSQ_RANDOM_SEEDS", "40"))))
 
 
 def _config(seed):
@@ -208,6 +208,10 @@ def test_random_configuration_fp32_vs_oracle(seed):
     r = _rel(eta_a, eta_b)
     print(f"seed {seed} ({skw['solver']}): fp32 eta rel-L2 {r:.3e}")
     assert r <= 1e-4
+    # the fp32 run's wetness is judged against its own (float-rounded) bed:
+    # a dry cell holds w == float(bed_eff) exactly, which sits a rounding
+    # step above or below the fp64 bed (tools/diag_fp32_mask.py, seed 50)
     h_dry = sim.h_dry
-    assert np.array_equal((sim.state.w - bathy.bed_eff)[ii] > h_dry,
+    bed32 = bathy.bed_eff.astype(np.float32).astype(np.float64)
+    assert np.array_equal((sim.state.w - bed32)[ii] > h_dry,
                           (ora.state.w - bathy.bed_eff)[ii] > h_dry)
