@@ -106,3 +106,36 @@ def test_spike_coupled_strips_golden_maker_sponge():
     scale = max(np.linalg.norm(z["p"][II]), np.linalg.norm(z["q"][II]))
     for f in ("p", "q"):
         assert np.linalg.norm(getattr(st, f)[II] - z[f][II]) / scale <= 1e-12, f
+
+
+@pytest.mark.parametrize("coupling,world", [("pipeline", 3), ("spike", 2)])
+def test_fp32_strips_match_single_grid_fp32(coupling, world):
+    """precision="fp32" on y-strips (the fp32 line of the multi-GPU bench):
+    the rank pipeline performs the one-grid fp32 operations exactly (bitwise
+    against the single-grid fp32 run), the spike coupling within fp32
+    rounding of it; and the strip run stays within the fp32 contract of the
+    fp64 one-grid reference (eta rel-L2 <= 1e-4, same wet mask)."""
+    case = make_case("C4", scale=8)
+
+    def mk(cls=stepper.Simulator, precision="fp32", **kw):
+        return cls(case.bathy, case.state.copy(), case.boundaries,
+                   stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
+                   precision=precision, **kw)
+    one32, one64 = mk(), mk(precision="fp64")
+    sp = mk(ShardedSimulator, world=world, coupling=coupling)
+    for _ in range(30):
+        a, b = one32.advance(), sp.advance()
+        one64.advance()
+        if coupling == "pipeline":
+            assert (a.dt, a.max_cfl, a.max_speed) == (b.dt, b.max_cfl, b.max_speed)
+    sa, sb, s64 = one32.state, sp.state, one64.state
+    if coupling == "pipeline":
+        for f in ("w", "p", "q"):
+            assert np.array_equal(getattr(sa, f), getattr(sb, f)), f
+    else:
+        assert _rel(sb.w[II], sa.w[II]) <= 1e-6
+    rest = np.maximum(case.bathy.ws, case.bathy.bed_eff)
+    assert _rel((sb.w - rest)[II], (s64.w - rest)[II]) <= 1e-4
+    bed32 = case.bathy.bed_eff.astype(np.float32).astype(np.float64)
+    h = sp.h_dry
+    assert np.array_equal((sb.w - bed32)[II] > h, (s64.w - case.bathy.bed_eff)[II] > h)
