@@ -856,6 +856,8 @@ struct Engine : EngineBase {
         h.sc = p->sc;
         h.sp = p->sp;
         h.sp2 = p->sp2;
+        h.f_dt = (float)h.dt, h.f_wc = (float)h.wc, h.f_wp = (float)h.wp, h.f_wp2 = (float)h.wp2;
+        h.f_sc = (float)h.sc, h.f_sp = (float)h.sp, h.f_sp2 = (float)h.sp2, h.f_pad_ = 0.f;
         h.spec = p->spec && !strip() ? 1 : 0;
         h.adaptive = p->adaptive;
         h.step_index = p->step_index;

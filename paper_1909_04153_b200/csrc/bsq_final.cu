@@ -246,6 +246,8 @@ static __device__ void spec_next(const DevParams &P, double max_rate, DevParams 
     N.dt = dt;
     N.euler = euler;
     N.wc = w0, N.wp = w1, N.wp2 = w2, N.sc = s0, N.sp = s1, N.sp2 = s2;
+    N.f_dt = (float)dt, N.f_wc = (float)w0, N.f_wp = (float)w1, N.f_wp2 = (float)w2;
+    N.f_sc = (float)s0, N.f_sp = (float)s1, N.f_sp2 = (float)s2;
     for (int s = 0; s < 4; s++) {  // the next step's ghosts at t are this step's at t + dt
         N.gw_t[s] = P.gw_n[s];
         N.gf_t[s] = P.gf_n[s];

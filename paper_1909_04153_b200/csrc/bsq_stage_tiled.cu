@@ -374,15 +374,15 @@ __global__ void __launch_bounds__(NT, stage_minb<T>()) k_stage(Consts<T> C, cons
     // predictor (stepper.py:239-250, 109-132; multistep.py:139-153)
     T wn, bu, bv, us, vs;
     if (P->euler) {
-        const T dt = T(P->dt);
+        const T dt = par<T>(P->dt, P->f_dt);
         wn = wc + dt * rw;
         bu = ustar + dt * rp;
         bv = vstar + dt * rq;
         us = bu;
         vs = bv;
     } else {
-        const T wc0 = T(P->wc), wp1 = T(P->wp), wp2 = T(P->wp2);
-        const T s0 = T(P->sc), s1 = T(P->sp), s2 = T(P->sp2);
+        const T wc0 = par<T>(P->wc, P->f_wc), wp1 = par<T>(P->wp, P->f_wp), wp2 = par<T>(P->wp2, P->f_wp2);
+        const T s0 = par<T>(P->sc, P->f_sc), s1 = par<T>(P->sp, P->f_sp), s2 = par<T>(P->sp2, P->f_sp2);
         wn = wc + (wc0 * rw + wp1 * A.h1[0][o] + wp2 * A.h2[0][o]);
         bu = ustar + (wc0 * rp + wp1 * A.h1[1][o] + wp2 * A.h2[1][o]);
         bv = vstar + (wc0 * rq + wp1 * A.h1[2][o] + wp2 * A.h2[2][o]);
