@@ -46,11 +46,14 @@ struct Red {
 };
 
 // per-thread accumulators in the kernel's precision: max is exact and the
-// conversion to double monotone, so the maxima equal the fp64-accumulated ones
+// conversion to double monotone, so the maxima equal the fp64-accumulated ones.
+// The clamped-volume tally too (fp64: the same double sum; fp32: a float sum
+// over the thread's cells, converted once -- a per-cell double add and
+// conversion ran on the fp64 pipe)
 template <class T>
 struct Acc {
     T rate, speed, depth, dev;
-    double clamp;
+    T clamp;
     int nan;
 };
 
@@ -94,7 +97,7 @@ __device__ __forceinline__ Red red_warp(const Acc<T> &a) {
     r.speed = double(warp_max_nonneg(a.speed));
     r.depth = double(warp_max_nonneg(a.depth));
     r.dev = double(warp_max_nonneg(a.dev));
-    r.clamp = warp_sum(a.clamp);
+    r.clamp = warp_sum(double(a.clamp));
     r.nan = __any_sync(0xffffffffu, a.nan);
     return r;
 }
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(FT, final_minb<T>()) k_final(Consts<T> C, Fina
     const int nx = L.nx, ny = L.ny;
     const bool sponges = (C.sponge_len[0] | C.sponge_len[1] | C.sponge_len[2] | C.sponge_len[3]) != 0;
     const long rstep = (long)FY * L.pitch;
-    Acc<T> r{T(0), T(0), T(0), T(0), 0.0, 0};
+    Acc<T> r{T(0), T(0), T(0), T(0), T(0), 0};
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int bx = tile % tiles_x, by = tile / tiles_x;
     const int I = GL + bx * FX + threadIdx.x;
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(FT, final_minb<T>()) k_final(Consts<T> C, Fina
             T p = vp[k], q = vq[k];
             // clamp and volume tally (stepper.py:281-285); np.maximum keeps NaN
             const T def = be - w;
-            if (def > T(0) || def != def) r.clamp = r.clamp + double(def);
+            if (def > T(0) || def != def) r.clamp = r.clamp + def;
             w = (w >= be || w != w) ? w : be;
             // film cutoff (stepper.py:288-292)
             if (C.h_dry > T(0) && (w - be) < C.h_dry) {
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(FT) k_extrema(Consts<T> C, const T *w, const T
                                                 const T *be, Partial *part) {
     const Layout L = C.L;
     const int I = GL + blockIdx.x * FX + threadIdx.x;
-    Acc<T> a{T(0), T(0), T(0), T(0), 0.0, 0};
+    Acc<T> a{T(0), T(0), T(0), T(0), T(0), 0};
     for (int k = 0; k < FR; k++) {
         const int J = GL + blockIdx.y * FR * FY + k * FY + threadIdx.y;
         if (I >= L.nx + GL || J >= L.ny + GL) continue;
