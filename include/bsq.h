@@ -189,7 +189,14 @@ int bsq_fill_ghosts(bsq_ctx *ctx, const double *maker_eta, const double *maker_f
  *   BSQ_PH_CORRECT cross-correction right-hand sides
  *   BSQ_PH_SOLVE2F, BSQ_PH_SOLVE2B  second solve, as above
  *   BSQ_PH_FINAL   finalize + reductions -> result (local; the host reduces
- *                  across ranks), synchronizes the stream */
+ *                  across ranks), synchronizes the stream
+ * Speculation on strips (params->spec): call BSQ_PH_FINAL_LAUNCH first (the
+ * finalize kernel alone), all-reduce (max) the first double of BSQ_ARR_RESULT
+ * -- the strip's max CFL rate -- over the ranks on the context's stream, then
+ * BSQ_PH_FINAL: the device controller turns the global rate into the next
+ * step's parameters and queues its ghosts at t and the stage's inner rows
+ * behind the result copy; the next step verifies them bit for bit (as
+ * bsq_step does) and runs only the stage's edge rows. */
 enum {
     BSQ_PH_GHOST = 0, BSQ_PH_STAGE = 1, BSQ_PH_SOLVE1F = 2, BSQ_PH_SOLVE1B = 3,
     BSQ_PH_CORRECT = 4, BSQ_PH_SOLVE2F = 5, BSQ_PH_SOLVE2B = 6, BSQ_PH_FINAL = 7,
@@ -198,7 +205,7 @@ enum {
      * halo is in flight), the EDGE phase the rest once the halo is in place
      * (and, for the stage, the predicted-state ghosts) */
     BSQ_PH_STAGE_INNER = 8, BSQ_PH_STAGE_EDGE = 9, BSQ_PH_CORRECT_INNER = 10,
-    BSQ_PH_CORRECT_EDGE = 11
+    BSQ_PH_CORRECT_EDGE = 11, BSQ_PH_FINAL_LAUNCH = 12
 };
 int bsq_phase(bsq_ctx *ctx, int phase, const bsq_step_params *params, bsq_step_result *result);
 /* cw of this strip's last row, per column (nx): the next strip's cw_south */
@@ -210,8 +217,10 @@ enum {
     BSQ_ARR_W = 0, BSQ_ARR_P = 1, BSQ_ARR_Q = 2,                /* committed state */
     BSQ_ARR_W_NEW = 3, BSQ_ARR_P_NEW = 4, BSQ_ARR_Q_NEW = 5,    /* pending state */
     BSQ_ARR_DW_IN = 6, BSQ_ARR_DW_OUT = 7, BSQ_ARR_X_IN = 8, BSQ_ARR_X_OUT = 9, /* nx vectors */
-    BSQ_ARR_Q2 = 10  /* scratch Q of the bsq_solve_momentum seam (the step itself solves
+    BSQ_ARR_Q2 = 10, /* scratch Q of the bsq_solve_momentum seam (the step itself solves
                         both times into BSQ_ARR_Q_NEW) */
+    BSQ_ARR_RESULT = 11  /* the step's device result; its first double is the max CFL
+                            rate (speculation on strips, see BSQ_PH_FINAL_LAUNCH) */
 };
 int bsq_array_layout(bsq_ctx *ctx, int array, size_t *byte_offset, int *pitch, int *xo,
                      int *elem_bytes);

@@ -47,8 +47,9 @@ class Static(ctypes.Structure):
 
 # phased step (y-strip sharding) and device array ids -- include/bsq.h
 PH_GHOST, PH_STAGE, PH_SOLVE1F, PH_SOLVE1B, PH_CORRECT, PH_SOLVE2F, PH_SOLVE2B, PH_FINAL = range(8)
-PH_STAGE_INNER, PH_STAGE_EDGE, PH_CORRECT_INNER, PH_CORRECT_EDGE = range(8, 12)
+PH_STAGE_INNER, PH_STAGE_EDGE, PH_CORRECT_INNER, PH_CORRECT_EDGE, PH_FINAL_LAUNCH = range(8, 13)
 ARR_Q2 = 10
+ARR_RESULT = 11
 ARR_W, ARR_P, ARR_Q, ARR_W_NEW, ARR_P_NEW, ARR_Q_NEW, ARR_DW_IN, ARR_DW_OUT, ARR_X_IN, ARR_X_OUT = \
     range(10)
 

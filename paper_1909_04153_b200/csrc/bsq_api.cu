@@ -9,6 +9,7 @@
 // contraction disabled (-ffp-contract=off), so it reproduces the reference's
 // numpy/numba values bit for bit (implicit.py:84-119, _kernels.py:360-378).
 #include <cmath>
+#include <cstddef>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -242,6 +243,8 @@ struct Engine : EngineBase {
     bool spec_pending = false;   // next step's ghost + stage are queued
     bool spec_commit = false;    // ... and the step they follow was committed
     bool spec_used = false;      // this step runs on them
+    int spec_lo = 0, spec_hi = 0;  // rows of the queued stage (a strip queues its inner rows)
+    bool final_split = false;    // BSQ_PH_FINAL_LAUNCH ran: the max rate was rank-reduced
     bsq_step_params last_p{};    // parameters of the step that queued them
     const bsq_step_params *cur_p = nullptr;  // the step in progress (bsq_step's argument)
     SpecNext spec_h{};           // their scheme parameters (device controller)
@@ -858,7 +861,7 @@ struct Engine : EngineBase {
         h.sp2 = p->sp2;
         h.f_dt = (float)h.dt, h.f_wc = (float)h.wc, h.f_wp = (float)h.wp, h.f_wp2 = (float)h.wp2;
         h.f_sc = (float)h.sc, h.f_sp = (float)h.sp, h.f_sp2 = (float)h.sp2, h.f_pad_ = 0.f;
-        h.spec = p->spec && !strip() ? 1 : 0;
+        h.spec = p->spec ? 1 : 0;
         h.adaptive = p->adaptive;
         h.step_index = p->step_index;
         h.cfl_target = p->cfl_target;
@@ -1030,7 +1033,7 @@ struct Engine : EngineBase {
             // a step abandoned after bsq_spike_fix(2) (e.g. a failed exchange)
             // must not hand its coupling correction to this step's k_final
             spike_fix_pending = false;
-            spec_used = !strip() && spec_matches(p);
+            spec_used = spec_matches(p);
             spec_pending = false;
             if (spec_used) {  // the stage already ran (on dpar[pk ^ 1])
                 pk ^= 1;
@@ -1075,6 +1078,8 @@ struct Engine : EngineBase {
                 launch_stage(C, dparams, A, 1, st, &sm);
                 fold_req = false;
                 ev_mark("stage");
+            } else {
+                stage_rest(slot);
             }
             ++step_launches;
             launch_ghost(C, dparams, 1, W(nxt), Pp(cur), Qq(cur), W(nxt), Pp(nxt), Qq(nxt), st);
@@ -1135,6 +1140,8 @@ struct Engine : EngineBase {
                 }
                 fold_req = false;
                 ev_mark("stage");
+            } else {
+                stage_rest(slot);
             }
             stage_inner = false;
             ++step_launches;
@@ -1189,6 +1196,10 @@ struct Engine : EngineBase {
                 ev_mark("solve2b");
             }
             break;
+        case BSQ_PH_FINAL_LAUNCH:
+            final_kernel(slot, nxt);
+            final_split = true;
+            break;
         case BSQ_PH_FINAL:
             return finish(r, slot, nxt);
         default:
@@ -1206,7 +1217,26 @@ struct Engine : EngineBase {
         return BSQ_OK;
     }
 
-    int finish(bsq_step_result *r, int slot, int nxt) {
+    // the rows of a speculated stage's step that the queued stage did not run
+    // (a strip queues only the rows that read no halo row)
+    void stage_rest(int slot) {
+        if (spec_lo <= 0 && spec_hi >= d.ny) return;
+        const StagePtrs<T> A = stage_ptrs(slot);
+        const StageMaps sm = stage_maps_for(A);
+        if (spec_lo > 0) {
+            ++step_launches;
+            launch_stage(C, dparams, A, 1, st, &sm, 0, spec_lo);
+        }
+        if (spec_hi < d.ny) {
+            ++step_launches;
+            launch_stage(C, dparams, A, 1, st, &sm, spec_hi, d.ny - spec_hi);
+        }
+        ev_mark("stage");
+    }
+
+    // k_final: the single-grid controller (spec_next in its last CTA) unless
+    // this is a strip, whose rate must first be reduced over the ranks
+    void final_kernel(int slot, int nxt) {
         FinalPtrs<T> F;
         F.w = W(nxt);
         F.pin = Pp(nxt);  // the last solve's result, in place
@@ -1227,12 +1257,22 @@ struct Engine : EngineBase {
         F.sp_south = d.south_internal;
         F.sp_north = d.north_internal;
         spike_fix_pending = false;
-        const bool spec = hparams->spec && !strip() && !fold_req;
         F.P = dparams;
-        F.pnext = spec ? dpar[pk ^ 1] : nullptr;
+        F.pnext = (hparams->spec && !strip() && !fold_req) ? dpar[pk ^ 1] : nullptr;
         ++step_launches;
         launch_final(C, F, st);
         ev_mark("final");
+    }
+
+    int finish(bsq_step_result *r, int slot, int nxt) {
+        if (!final_split) final_kernel(slot, nxt);
+        // a strip speculates only when the host reduced the rate in between
+        const bool spec = hparams->spec && !fold_req && (!strip() || final_split);
+        final_split = false;
+        if (spec && strip()) {
+            ++step_launches;
+            launch_spec_next(dparams, dres, dpar[pk ^ 1], st);
+        }
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(hres, dres, sizeof(DevResult), cudaMemcpyDeviceToHost, st));
         if (ng)
@@ -1262,11 +1302,19 @@ struct Engine : EngineBase {
             frame_w = W(nxt), frame_p = Pp(nxt), frame_q = Qq(nxt);
             frame_restored = false;
             pre("ghost_t");
-            ++step_launches;
             const StagePtrs<T> A = stage_ptrs_on(W(nxt), Pp(nxt), Qq(nxt), (slot + 1) % 4, slot, head,
                                                  Wspare());
             const StageMaps sm = stage_maps_for(A);
-            launch_stage(C, pn, A, 1, st, &sm);
+            // a strip: the rows that read no halo row (the next step's
+            // exchange has not happened); the edge rows run in that step
+            if (strip()) inner_rows(2, spec_lo, spec_hi);
+            else spec_lo = 0, spec_hi = d.ny;
+            if (spec_hi > spec_lo) {
+                ++step_launches;
+                launch_stage(C, pn, A, 1, st, &sm, spec_lo, spec_hi - spec_lo);
+            } else {
+                spec_lo = spec_hi = 0;  // nothing queued: the next step runs every row
+            }
             pre("stage");
             CU(cudaGetLastError());
             spec_pending = true;
@@ -1335,6 +1383,13 @@ struct Engine : EngineBase {
         case BSQ_ARR_X_IN: ptr = x_in; break;
         case BSQ_ARR_X_OUT: ptr = x_out; break;
         case BSQ_ARR_Q2: ptr = arr[A_Q2]; break;
+        case BSQ_ARR_RESULT:  // DevResult: max_rate (a double) first
+            static_assert(offsetof(DevResult, max_rate) == 0, "max_rate leads DevResult");
+            *off = (size_t)((const char *)dres - base);
+            *pitch = 1;
+            *xo = 0;
+            *eb = (int)sizeof(double);
+            return BSQ_OK;
         default: return fail(BSQ_ERR_BAD_ARG, "unknown array id");
         }
         *off = (size_t)((const char *)ptr - base);

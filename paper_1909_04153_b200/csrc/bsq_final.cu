@@ -395,6 +395,18 @@ __global__ void __launch_bounds__(FT, final_minb<T>()) k_final(Consts<T> C, Fina
     }
 }
 
+// The device controller for a y-strip: the same spec_next as k_final's last
+// CTA, on the max rate the host has all-reduced over the ranks in place
+// (res->max_rate) -- k_final alone only sees the strip's own maximum.
+#if BSQ_INST_F64
+static __global__ void k_spec_next(const DevParams *P, DevResult *res, DevParams *N) {
+    if (threadIdx.x == 0 && P->spec) spec_next(*P, res->max_rate, *N, res->next);
+}
+void launch_spec_next(const DevParams *P, DevResult *res, DevParams *N, cudaStream_t st) {
+    k_spec_next<<<1, 32, 0, st>>>(P, res, N);
+}
+#endif
+
 // speed_extrema of a committed state (construction time, stepper.py:210)
 template <class T>
 __global__ void __launch_bounds__(FT) k_extrema(Consts<T> C, const T *w, const T *p, const T *q,

@@ -158,6 +158,8 @@ void launch_correct(const Consts<T> &C, const CorrectPtrs<T> &K, cudaStream_t st
                     int nrows = -1);
 template <class T>
 void launch_final(const Consts<T> &C, const FinalPtrs<T> &F, cudaStream_t st);
+// a strip's device controller on the rank-reduced max rate (res->max_rate)
+void launch_spec_next(const DevParams *P, DevResult *res, DevParams *N, cudaStream_t st);
 template <class T>
 void launch_extrema(const Consts<T> &C, const T *w, const T *p, const T *q, const T *be,
                     Partial *part, cudaStream_t st);

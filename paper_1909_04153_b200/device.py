@@ -177,6 +177,11 @@ class DeviceStep:
         n = (self.ny + 4) * pitch * eb
         return self.workspace[off:off + n].view(dt).view(self.ny + 4, pitch)[:, xo:xo + self.nx + 4]
 
+    def result_rate(self) -> torch.Tensor:
+        """Torch view of the device step result's max CFL rate (one double)."""
+        off, _, _, _ = self._layout(nat.ARR_RESULT)
+        return self.workspace[off:off + 8].view(torch.float64)
+
     def vector(self, which: int) -> torch.Tensor:
         """Torch view of an nx-long device vector (strip boundary values)."""
         off, _, _, eb = self._layout(which)

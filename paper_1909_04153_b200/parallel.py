@@ -151,6 +151,15 @@ class LocalComm:
     def gather_spike_table(self, per: dict, nx: int) -> np.ndarray:
         return np.stack([per[r] for r in range(self.world)])
 
+    def max_rate(self, strips, stream) -> None:
+        """Every strip's device max CFL rate <- the max over the strips
+        (stream-ordered; max is exact, so this equals the host fold)."""
+        with torch.cuda.stream(stream):
+            vs = [strips[r].result_rate() for r in sorted(strips)]
+            m = torch.stack(vs).amax(0)
+            for v in vs:
+                v.copy_(m)
+
     def spike_bounds(self, strips, arr: int, stream) -> dict:
         with torch.cuda.stream(stream):
             parts = []
@@ -361,6 +370,17 @@ class DistComm:
         bufs = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(bufs, t, group=self.group)
         return np.stack([b.cpu().numpy() for b in bufs])
+
+    def max_rate(self, strips, stream) -> None:
+        """All-reduce (max) of this rank's device max CFL rate, in place on
+        the library stream (NCCL reads device memory; gloo stages through the
+        host)."""
+        v = strips[self.rank].result_rate()
+        with torch.cuda.stream(stream):
+            wire = self._wire(v)
+            self.dist.all_reduce(wire, op=self.dist.ReduceOp.MAX, group=self.group)
+            if wire is not v:
+                v.copy_(wire)
 
     def spike_bounds(self, strips, arr: int, stream) -> dict:
         s = strips[self.rank]
@@ -594,6 +614,13 @@ class ShardedDevice:
         self.comm.halo(strips, _PENDING_PQ, 1, self.stream, inner=each(nat.PH_CORRECT_INNER))
         each(nat.PH_CORRECT_EDGE)()
         self._ysolve(2)
+        if params.spec:
+            # speculation: k_final alone, the max CFL rate reduced over the
+            # ranks on the device, then PH_FINAL's device controller queues the
+            # next step's ghosts and inner stage rows behind the result copy
+            for r in order:
+                strips[r].phase(nat.PH_FINAL_LAUNCH)
+            self.comm.max_rate(strips, self.stream)
         parts = []
         for r in order:
             _, res = strips[r].phase(nat.PH_FINAL)

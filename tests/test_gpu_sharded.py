@@ -139,3 +139,35 @@ def test_fp32_strips_match_single_grid_fp32(coupling, world):
     bed32 = case.bathy.bed_eff.astype(np.float32).astype(np.float64)
     h = sp.h_dry
     assert np.array_equal((sb.w - bed32)[II] > h, (s64.w - case.bathy.bed_eff)[II] > h)
+
+
+@pytest.mark.parametrize("coupling,world", [("pipeline", 3), ("spike", 2)])
+def test_strip_speculation_changes_no_bit(coupling, world):
+    """Strips queue the next step's ghosts and inner stage rows on the rank-
+    reduced CFL rate (BSQ_PH_FINAL_LAUNCH); the run with speculation equals the
+    run without it bit for bit, with state reads (ghost frame restores) and an
+    in-place edit in between."""
+    case = make_case("C4", scale=8)
+
+    def run(spec):
+        sim = ShardedSimulator(case.bathy, case.state.copy(), case.boundaries,
+                               stepper.TimeController(dt_init=case.dt_init), phys=case.phys,
+                               world=world, coupling=coupling)
+        sim.speculate = spec
+        recs = []
+        for k in range(24):
+            recs.append(sim.advance())
+            if k in (5, 11):
+                st = sim.state
+                _ = st.w.sum()
+            if k == 15:
+                sim.state.p[200:210, 300:310] *= 0.5
+        out = (recs, [getattr(sim.state, f).copy() for f in ("w", "p", "q")])
+        sim.close()
+        return out
+
+    r1, s1 = run(True)
+    r0, s0 = run(False)
+    assert r1 == r0
+    for a, b in zip(s1, s0):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))

@@ -33,6 +33,10 @@ class FakeStrip:
         self.v = {a: torch.zeros(NX, dtype=torch.float64)
                   for a in (nat.ARR_DW_IN, nat.ARR_DW_OUT, nat.ARR_X_IN, nat.ARR_X_OUT)}
         self.col = torch.zeros(NX, dtype=torch.float64)
+        self.rate = torch.tensor([0.75 + 0.5 * rank], dtype=torch.float64)
+
+    def result_rate(self):
+        return self.rate
 
     def rows(self, a):
         return self.f[a]
@@ -115,9 +119,11 @@ def _worker(rank, port, out_q):
         # spike coupling: static table once, first/last solved rows per solve
         table = comm.gather_spike_table({rank: _spike_coef(rank)}, NX)
         yb = comm.spike_bounds(strips, nat.ARR_Q_NEW, None)[rank].numpy().copy()
+        # speculation on strips: the step's max CFL rate reduced in place
+        comm.max_rate(strips, None)
         out_q.put((rank, {a: t.numpy().copy() for a, t in s.f.items()}, s.col.numpy().copy(),
                    red, [a.copy() for a in full], got_tail, any_flag, table, yb,
-                   [t.numpy() for t in seen]))
+                   [t.numpy() for t in seen], float(s.rate[0])))
     finally:
         dist.destroy_process_group()
 
@@ -224,3 +230,15 @@ def test_combine_matches_reference_semantics():
     m = _combine([a, b], 4, [0, 3])
     assert m["max_rate"] == 3.0 and m["clamped"] == 4.0
     assert m["stage_bad"][0] == 11  # min(11, 0 + 3*4 = 12)
+
+
+def test_max_rate_reduced_in_place_on_every_strip(dist_results):
+    """The device controller of each strip sees the global max rate (the value
+    the host fold of the step results computes)."""
+    want = 0.75 + 0.5 * (WORLD - 1)
+    for r in range(WORLD):
+        assert dist_results[r][9] == want
+    ranges = split_rows(NY, WORLD)
+    strips = {r: FakeStrip(r, *ranges[r]) for r in range(WORLD)}
+    LocalComm(WORLD).max_rate(strips, None)
+    assert all(float(s.rate[0]) == want for s in strips.values())

@@ -32,10 +32,12 @@ print(f"one grid 4096^2: {timed(one):.3f} ms/step", flush=True)
 one.close()
 c2 = make_case("C5", gpus=2)
 for coupling in ("spike", "pipeline"):
-    sp = ShardedSimulator(c2.bathy, c2.state.copy(), c2.boundaries,
-                          stepper.TimeController(dt_init=c2.dt_init), phys=c2.phys,
-                          world=2, coupling=coupling)
-    t = timed(sp)
-    print(f"2 strips of 4096^2 ({coupling}): {t:.3f} ms/step on one GPU = {t / 2:.3f} per strip",
-          flush=True)
-    sp.close()
+    for spec in (True, False):
+        sp = ShardedSimulator(c2.bathy, c2.state.copy(), c2.boundaries,
+                              stepper.TimeController(dt_init=c2.dt_init), phys=c2.phys,
+                              world=2, coupling=coupling)
+        sp.speculate = spec
+        t = timed(sp)
+        print(f"2 strips of 4096^2 ({coupling}, speculate={spec}): {t:.3f} ms/step on one GPU "
+              f"= {t / 2:.3f} per strip", flush=True)
+        sp.close()
