@@ -236,11 +236,14 @@ int bsq_pivot_flags(bsq_ctx *ctx, int *all_positive, int *singular);
  * Per solve (after BSQ_PH_SOLVE1F or BSQ_PH_SOLVE2F): gather every rank's
  * first and last solved row of Q (BSQ_ARR_Q_NEW: both solves land in the
  * pending Q) into a device array G x 2 x nx of the context's precision, then
- * bsq_spike_fix(solve, ...) solves the coupling system per column.  Solve 1's
- * correction is applied to Q in place on the library stream.  Solve 2's is
- * deferred: BSQ_PH_FINAL applies it as k_final loads Q, so the pending Q
- * is the coupled solution only after BSQ_PH_FINAL (a new BSQ_PH_GHOST drops
- * a correction that never reached BSQ_PH_FINAL). */
+ * bsq_spike_fix(solve, ...) solves the coupling system per column and
+ * corrects Q in place on the library stream, on the rows where the strip's
+ * spikes are not negligible (|v|, |w| >= 2^-64 at setup: the rows near the
+ * internal sides; elsewhere the dropped terms are below 2^-64 of the
+ * interface values).  A build with -DBSQ_SPIKE2_IN_FINAL=1 defers solve 2's
+ * correction into BSQ_PH_FINAL (k_final applies it as it loads Q; the
+ * pending Q is then the coupled solution only after BSQ_PH_FINAL, and a new
+ * BSQ_PH_GHOST drops a correction that never reached it). */
 int bsq_spike_coeffs(bsq_ctx *ctx, double *out);
 int bsq_set_spike_table(bsq_ctx *ctx, const double *table, int nranks, int rank);
 int bsq_spike_fix(bsq_ctx *ctx, int solve, const void *ybound_device);

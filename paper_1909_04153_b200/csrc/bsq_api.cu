@@ -22,6 +22,10 @@
 
 #include <nvtx3/nvToolsExt.h>
 
+#ifndef BSQ_SPIKE2_IN_FINAL
+#define BSQ_SPIKE2_IN_FINAL 0
+#endif
+
 #include "../../include/bsq.h"
 #include "bsq_launch.h"
 
@@ -514,6 +518,11 @@ struct Engine : EngineBase {
     // every column of this strip's block, with the block's own LU factors
     // (thomas_batch's recurrence on a unit right-hand side)
     std::vector<double> sp_coef;  // 4 x nx: v_first, v_last, w_first, w_last
+    // rows [0, sp_jv) carry the south spike v and rows [sp_jw, ny) the north
+    // spike w at magnitudes >= SPIKE_TINY; beyond them the corrections
+    // (|v b|, |w t| < 2^-64 of the interface values) are dropped
+    static constexpr double SPIKE_TINY = 0x1p-64;
+    int sp_jv = 0, sp_jw = 0;
     void make_spikes(const std::vector<T> &ay, const std::vector<T> &deny,
                      const std::vector<T> &cwy, const std::vector<T> &cyl) {
         const int nx = d.nx, ny = d.ny;
@@ -521,6 +530,8 @@ struct Engine : EngineBase {
         std::vector<T> vv(E, T(0)), ww(E, T(0));
         std::vector<double> col(ny);
         sp_coef.assign(4 * (size_t)nx, 0.0);
+        sp_jv = 0;
+        sp_jw = ny;
         for (int i = 0; i < nx; i++) {
             auto at = [&](int j) { return L.at(j + GL, i + GL); };
             if (d.south_internal) {
@@ -532,6 +543,11 @@ struct Engine : EngineBase {
                 }
                 for (int j = ny - 2; j >= 0; j--) col[j] = col[j] - double(cwy[at(j)]) * col[j + 1];
                 for (int j = 0; j < ny; j++) vv[at(j)] = T(col[j]);
+                for (int j = ny - 1; j >= sp_jv; j--)
+                    if (!(std::fabs(double(T(col[j]))) < SPIKE_TINY)) {  // NaN counts as large
+                        sp_jv = j + 1;
+                        break;
+                    }
                 sp_coef[0 * (size_t)nx + i] = double(T(col[0]));
                 sp_coef[1 * (size_t)nx + i] = double(T(col[ny - 1]));
             }
@@ -539,10 +555,18 @@ struct Engine : EngineBase {
                 col[ny - 1] = double(cyl[i]) / double(deny[at(ny - 1)]);
                 for (int j = ny - 2; j >= 0; j--) col[j] = 0.0 - double(cwy[at(j)]) * col[j + 1];
                 for (int j = 0; j < ny; j++) ww[at(j)] = T(col[j]);
+                for (int j = 0; j < sp_jw; j++)
+                    if (!(std::fabs(double(T(col[j]))) < SPIKE_TINY)) {
+                        sp_jw = j;
+                        break;
+                    }
                 sp_coef[2 * (size_t)nx + i] = double(T(col[0]));
                 sp_coef[3 * (size_t)nx + i] = double(T(col[ny - 1]));
             }
         }
+        if (std::getenv("BSQ_SPIKE_VERBOSE"))
+            std::fprintf(stderr, "bsq spike cut-offs: v rows [0, %d), w rows [%d, %d)\n",
+                         d.south_internal ? sp_jv : 0, d.north_internal ? sp_jw : ny, ny);
         cudaMemcpyAsync(arr[A_SPV], vv.data(), sizeof(T) * E, cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(arr[A_SPW], ww.data(), sizeof(T) * E, cudaMemcpyHostToDevice, st);
         cudaStreamSynchronize(st);
@@ -573,11 +597,15 @@ struct Engine : EngineBase {
         if ((solve != 1 && solve != 2) || !ybound) return fail(BSQ_ERR_BAD_ARG, "bad spike_fix args");
         T *x = Qq(1 - cur);  // both solves land in the pending Q
         T *bt = (T *)(base + offs[A_COUNT + S_SPBT]);
-        // the second solve's correction is applied by k_final as it loads Q
-        // (same operations as k_spike_fix, one pass over the strip less)
+        // BSQ_SPIKE2_IN_FINAL: the second solve's correction applied by
+        // k_final as it loads Q (same operations as k_spike_fix).  Off: with
+        // the cut-off rows the pass covers only the rows near the interfaces
+        // (≈47 % of a 4096-row strip), and k_final's spike instantiation
+        // spills (0.190 vs 0.134 ms); the pass costs 0.033 ms.
+        const bool in_final = solve == 2 && BSQ_SPIKE2_IN_FINAL;
         launch_spike(C, sp_G, sp_rank, d_sptab, (const T *)ybound, bt, x, arr[A_SPV], arr[A_SPW],
-                     d.south_internal, d.north_internal, st, solve == 1);
-        spike_fix_pending = solve == 2;
+                     d.south_internal, d.north_internal, st, !in_final, sp_jv, sp_jw);
+        spike_fix_pending = in_final;
         CU(cudaGetLastError());
         return BSQ_OK;
     }
@@ -1256,6 +1284,8 @@ struct Engine : EngineBase {
         F.spw = arr[A_SPW];
         F.sp_south = d.south_internal;
         F.sp_north = d.north_internal;
+        F.sp_jv = sp_jv;
+        F.sp_jw = sp_jw;
         spike_fix_pending = false;
         F.P = dparams;
         F.pnext = (hparams->spec && !strip() && !fold_req) ? dpar[pk ^ 1] : nullptr;

@@ -303,9 +303,10 @@ __global__ void __launch_bounds__(FT, final_minb<T>()) k_final(Consts<T> C, Fina
                 const bool in = iin && J0 + (k0 + k) * FY < ny + GL;
                 const long o = in ? o0 + (k0 + k) * rstep : L.at(GL, GL);
                 const int ic = iin ? I - GL : 0;  // no read past the 2*nx bound rows
+                const int jr = J0 + (k0 + k) * FY - GL;  // strip row (the spikes' cut-offs)
                 T r = vq[k];
-                if (F.sp_south) r = r - F.spv[o] * F.spbt[ic];
-                if (F.sp_north) r = r - F.spw[o] * F.spbt[nx + ic];
+                if (F.sp_south && jr < F.sp_jv) r = r - F.spv[o] * F.spbt[ic];
+                if (F.sp_north && jr >= F.sp_jw) r = r - F.spw[o] * F.spbt[nx + ic];
                 vq[k] = r;
             }
         }

@@ -114,6 +114,7 @@ struct FinalPtrs {
     // (q - v b_prev - w t_next, k_spike_fix's operations) instead of a pass
     const T *spv, *spw, *spbt;      // null: no correction pending
     int sp_south, sp_north;
+    int sp_jv, sp_jw;               // rows [0, sp_jv) take v, rows [sp_jw, ny) take w
 };
 
 // save != nullptr: each ghost cell's previous value goes to save first, in
@@ -170,7 +171,7 @@ int final_rows(int nx, int ny);  // k_final grid rows: row partials + counters
 template <class T>
 void launch_spike(const Consts<T> &C, int G, int rank, const double *table, const T *yb, T *bt,
                   T *x, const T *v, const T *w, int south, int north, cudaStream_t st,
-                  int apply = 1);
+                  int apply, int jv, int jw);
 // observers: gauge gather and the running max of w
 template <class T>
 void launch_gather(const T *w, const T *p, const T *q, const long long *goff, int ng, T *gval,

@@ -75,40 +75,54 @@ __global__ void k_spike_reduce(int nx, int G, int rank, const double *table, con
     bt[nx + i] = T(t_next);
 }
 
-// x = (y - v b_prev) - w t_next over the strip's interior, in place
+// x = (y - v b_prev) - w t_next over rows [j0, j1) of the strip, in place.
+// v is negligible from row jv on and w below row jw (|spike| < 2^-64
+// everywhere there, SPIKE_TINY in bsq_api.cu): those terms are dropped.
 template <class T>
 __global__ void k_spike_fix(Consts<T> C, T *x, const T *v, const T *w, const T *bt, int south,
-                            int north) {
+                            int north, int j0, int j1, int jv, int jw) {
     const Layout L = C.L;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y * blockDim.y + threadIdx.y;
-    if (i >= L.nx || j >= L.ny) return;
+    const int j = j0 + blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= L.nx || j >= j1) return;
     const long o = L.at(GL + j, GL + i);
     T r = x[o];
-    if (south) r = r - v[o] * bt[i];
-    if (north) r = r - w[o] * bt[L.nx + i];
+    if (south && j < jv) r = r - v[o] * bt[i];
+    if (north && j >= jw) r = r - w[o] * bt[L.nx + i];
     x[o] = r;
 }
 
 template <class T>
 void launch_spike(const Consts<T> &C, int G, int rank, const double *table, const T *yb, T *bt,
                   T *x, const T *v, const T *w, int south, int north, cudaStream_t st,
-                  int apply) {
+                  int apply, int jv, int jw) {
     k_spike_reduce<T><<<(C.L.nx + 127) / 128, 128, 0, st>>>(C.L.nx, G, rank, table, yb, bt);
     if (!apply) return;
-    dim3 blk(32, 8), grd((C.L.nx + 31) / 32, (C.L.ny + 7) / 8);
-    k_spike_fix<T><<<grd, blk, 0, st>>>(C, x, v, w, bt, south, north);
+    const int ny = C.L.ny;
+    if (!south) jv = 0;
+    if (!north) jw = ny;
+    auto rows = [&](int j0, int j1) {
+        if (j1 <= j0) return;
+        dim3 blk(32, 8), grd((C.L.nx + 31) / 32, (j1 - j0 + 7) / 8);
+        k_spike_fix<T><<<grd, blk, 0, st>>>(C, x, v, w, bt, south, north, j0, j1, jv, jw);
+    };
+    if (jv < jw) {  // two bands near the interfaces, the rows between untouched
+        rows(0, jv);
+        rows(jw, ny);
+    } else {
+        rows(0, ny);
+    }
 }
 
 #if BSQ_INST_F64
 template void launch_spike<double>(const Consts<double> &, int, int, const double *,
                                    const double *, double *, double *, const double *,
-                                   const double *, int, int, cudaStream_t, int);
+                                   const double *, int, int, cudaStream_t, int, int, int);
 #endif
 #if BSQ_INST_F32
 template void launch_spike<float>(const Consts<float> &, int, int, const double *, const float *,
                                   float *, float *, const float *, const float *, int, int,
-                                  cudaStream_t, int);
+                                  cudaStream_t, int, int, int);
 #endif
 
 }  // namespace bsq
