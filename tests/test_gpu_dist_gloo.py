@@ -91,3 +91,46 @@ def test_sharded_two_processes_match_one_grid(coupling, tmp_path):
         for f in ("w", "p", "q"):
             a, b = getattr(st, f), z[f]
             assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(a), f
+
+
+def _nccl_worker(rank, port, steps, path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_1909_04153_b200 import stepper
+    from paper_1909_04153_b200.parallel import DistComm, ShardedSimulator
+    from paper_1909_04153_b200.scenario import make_case
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    comm = DistComm()
+    assert not comm.staged  # device tensors go to NCCL directly
+    case = make_case("C4", scale=16)
+    sim = ShardedSimulator(case.bathy, case.state.copy(), case.boundaries,
+                           stepper.TimeController(dt_init=case.dt_init), phys=case.phys, comm=comm)
+    recs = [sim.advance() for _ in range(steps)]
+    st = sim.state
+    np.savez(path, w=st.w, p=st.p, q=st.q,
+             rec=np.array([(r.dt, r.max_cfl, r.max_speed, r.max_depth) for r in recs]))
+    dist.destroy_process_group()
+
+
+def test_nccl_single_rank_sharded_step_matches_one_grid(tmp_path):
+    """The NCCL transport on the one GPU a box has: a single-rank process
+    group drives the sharded step (NCCL all-reduce of the device CFL rate on a
+    workspace view, all_gather of the step results) and equals the single-grid
+    Simulator bitwise."""
+    from paper_1909_04153_b200 import stepper
+    from paper_1909_04153_b200.scenario import make_case
+    steps = 12
+    path = str(tmp_path / "nccl.npz")
+    mp.spawn(_nccl_worker, args=(_port(), steps, path), nprocs=1, join=True)
+    z = np.load(path)
+    case = make_case("C4", scale=16)
+    sim = stepper.Simulator(case.bathy, case.state.copy(), case.boundaries,
+                            stepper.TimeController(dt_init=case.dt_init), phys=case.phys)
+    recs = np.array([(r.dt, r.max_cfl, r.max_speed, r.max_depth)
+                     for r in (sim.advance() for _ in range(steps))])
+    assert np.array_equal(recs, z["rec"])
+    for f in ("w", "p", "q"):
+        assert np.array_equal(getattr(sim.state, f).view(np.uint64), z[f].view(np.uint64)), f
