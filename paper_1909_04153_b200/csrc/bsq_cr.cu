@@ -13,6 +13,7 @@
 // raise first -- solve phase, x before y, line, then reduction / core /
 // back substitution -- so the host reports the same ZeroDivisionError.
 #include <cstdint>
+#include <cstdlib>
 
 #include "bsq_device.cuh"
 #include "bsq_launch.h"
@@ -38,7 +39,9 @@ template <class T, bool XDIR>
 __device__ void cr_line(const Consts<T> &C, const CrPtrs<T> &K, int line, T *sm, int n2) {
     const Layout L = C.L;
     const int n = XDIR ? L.nx : L.ny;
-    T *a = sm, *b = sm + n2, *c = sm + 2 * n2, *r = sm + 3 * n2, *x = sm + 4 * n2;
+    // x overwrites r: a back-substitution level reads r only of the rows it
+    // solves (and x of coarser rows), the core reads both r before writing
+    T *a = sm, *b = sm + n2, *c = sm + 2 * n2, *r = sm + 3 * n2, *x = r;
     const T *A = XDIR ? K.ax : K.ay;
     const T *B = XDIR ? K.bx : K.by;
     const T *Cc = XDIR ? K.cx : K.cy;
@@ -110,8 +113,10 @@ __device__ void cr_line(const Consts<T> &C, const CrPtrs<T> &K, int line, T *sm,
         const int i1 = crs(n2 / 2 - 1), i2 = crs(n2 - 1);
         const T det = b[i1] * b[i2] - c[i1] * a[i2];
         if (det == T(0) && kind > 1) kind = 1;
-        x[i1] = (r[i1] * b[i2] - c[i1] * r[i2]) / det;
-        x[i2] = (b[i1] * r[i2] - a[i2] * r[i1]) / det;
+        const T x1 = (r[i1] * b[i2] - c[i1] * r[i2]) / det;
+        const T x2 = (b[i1] * r[i2] - a[i2] * r[i1]) / det;
+        x[i1] = x1;
+        x[i2] = x2;
     }
     __syncthreads();
     // back substitution (_kernels.py:442-449)
@@ -131,11 +136,29 @@ __device__ void cr_line(const Consts<T> &C, const CrPtrs<T> &K, int line, T *sm,
     for (int i = threadIdx.x; i < n; i += blockDim.x) out[off(i)] = x[crs(i)];
 }
 
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <class T>
 __global__ void __launch_bounds__(CR_THREADS) k_cr(Consts<T> C, CrPtrs<T> K, int nbx, int n2x,
-                                                   int n2y) {
+                                                   int n2y, int ahead) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *sm = reinterpret_cast<T *>(smem_raw);
+    // the line `ahead` CTAs later in launch order (about the next one this
+    // SM runs): its contiguous operands towards L2 while this line reduces
+    const int nl = (int)blockIdx.x + ahead;
+    if (ahead > 0 && threadIdx.x < 4 && nl < (int)gridDim.x) {
+        const Layout L = C.L;
+        const int k = threadIdx.x;
+        if (nl < nbx) {  // x line: a, b, c, r rows of the padded layout
+            const T *src = k == 0 ? K.ax : k == 1 ? K.bx : k == 2 ? K.cx : K.rx;
+            bulk_prefetch_l2(src + L.at(GL + nl, GL), (unsigned)(L.nx * sizeof(T)) & ~15u);
+        } else if (k < 3) {  // y line: the transposed diagonals (r is strided)
+            const T *src = k == 0 ? K.ay : k == 1 ? K.by : K.cy;
+            bulk_prefetch_l2(src + (long)(nl - nbx) * L.ny, (unsigned)(L.ny * sizeof(T)) & ~15u);
+        }
+    }
     if ((int)blockIdx.x < nbx)
         cr_line<T, true>(C, K, blockIdx.x, sm, n2x);
     else
@@ -151,7 +174,7 @@ static int pow2_at_least(int n) {
 #if BSQ_INST_F64
 size_t cr_smem_bytes(int nx, int ny, int elem) {
     const int n2 = pow2_at_least(nx > ny ? nx : ny);
-    return (size_t)5 * n2 * elem;
+    return (size_t)4 * n2 * elem;
 }
 #endif
 
@@ -168,7 +191,19 @@ void launch_cr(const Consts<T> &C, const CrPtrs<T> &K, cudaStream_t st) {
     const int cap = n2 >= 4096 ? CR_THREADS : 512;
     int threads = n2 / 2 < cap ? n2 / 2 : cap;
     threads = threads < 64 ? 64 : (threads + 31) / 32 * 32;
-    k_cr<T><<<C.L.ny + C.L.nx, threads, smem, st>>>(C, K, C.L.ny, n2x, n2y);
+    // CTAs resident at once (one line per SM at 4096 rows): the prefetch
+    // distance.  The occupancy depends on the line length, so per launch.
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cr<T>, threads, smem);
+    // only when one line fills an SM (4096 rows: 1.245 -> 1.174 ms per
+    // solve); with several lines per SM they hide each other's loads (1024
+    // rows: 0.0676 -> 0.069 with the prefetch)
+    int ahead = per <= 1 ? sms : 0;
+    static const char *env_ahead = std::getenv("BSQ_CR_AHEAD");  // A/B: 0 disables
+    if (env_ahead) ahead = std::atoi(env_ahead);
+    k_cr<T><<<C.L.ny + C.L.nx, threads, smem, st>>>(C, K, C.L.ny, n2x, n2y, ahead);
 }
 
 #if BSQ_INST_F64
