@@ -22,6 +22,9 @@ __device__ __forceinline__ unsigned long long bits(double v) {
 __device__ __forceinline__ unsigned long long bits(float v) { return __float_as_uint(v); }
 __device__ __forceinline__ bool bits_nonzero(double v) { return bits(v) != 0ull; }
 
+#ifndef BSQ_FINAL_F32_MULQ
+#define BSQ_FINAL_F32_MULQ 1
+#endif
 #ifndef BSQ_FINAL_FR
 #define BSQ_FINAL_FR 8
 #endif
@@ -143,8 +146,16 @@ __device__ __forceinline__ void extrema_cell(const Consts<T> &C, T w, T p, T q, 
     // both quotients correctly rounded via one reciprocal (branch-free when
     // h_eps is in rcp_rn_inrange's range: bsq_device.cuh flux_fast_rcp_ok)
     const T nrh = -(FAST ? rcp_depth(hstar) : rcp_rn(hstar));
-    T su = div_nonneg(fabs(p), hstar, nrh) + c;
-    T sv = div_nonneg(fabs(q), hstar, nrh) + c;
+    T su, sv;
+    if constexpr (sizeof(T) == 4 && BSQ_FINAL_F32_MULQ) {
+        // fp32 (a tolerance contract): the speeds only feed the CFL maxima,
+        // so the quotients are products with the reciprocal
+        su = fabs(p) * -nrh + c;
+        sv = fabs(q) * -nrh + c;
+    } else {
+        su = div_nonneg(fabs(p), hstar, nrh) + c;
+        sv = div_nonneg(fabs(q), hstar, nrh) + c;
+    }
     if (EXT && (tiny_nz(p, TINY_NUM) | tiny_nz(q, TINY_NUM))) {  // exact_tiny: under Markstein's range
         const T rh = -nrh;
         if (tiny_nz(p, TINY_NUM)) su = div_tiny_exact(fabs(p), hstar, rh) + c;
